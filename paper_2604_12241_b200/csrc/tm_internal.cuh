@@ -1,0 +1,146 @@
+// tm_internal.cuh — shared declarations of the B200 mining engine.
+//
+// Device layout of a built graph (all arrays resident in HBM, int32 ids):
+//
+//   edge table       e_src/e_dst int32[E], e_rank uint32[E]
+//   time ranks       uniq_time int64[R]: sorted distinct timestamps; every
+//                    time is stored as its dense rank, so a window
+//                    [t - delta, t] becomes the rank interval
+//                    [lower_bound(uniq_time, t - delta), rank(t)] (exact,
+//                    order preserving; txgraph.py:5-6 int64 ticks)
+//   dual CSR         per direction d (0 = in, 1 = out): ptr int32[N+1];
+//                    entries sorted by (owner, rank, eid) exactly as
+//                    np.lexsort((eid, time, owner)) (txgraph.py:134-144):
+//                    nbr int32[E], rnk uint32[E], eid int32[E]
+//   pair index       same runs re-sorted by (owner, nbr, rank, eid):
+//                    pkey uint64[E] = nbr << rank_bits | rank; c2p int32[E]
+//                    maps a CSR position to its pair position.  It answers
+//                    "edge a->b inside the window?" with one bisection and
+//                    "is CSR entry j the first occurrence of its neighbour in
+//                    the window?" (np.unique dedup, kernels.py:59) with one
+//                    load of the pair predecessor.
+//   self-loop flags  loop uint8[N] (txgraph.py:146-153 self-loop CSR)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+#include <string>
+
+#include "../../include/tempmine_b200.h"
+
+namespace tmb {
+
+constexpr int kMaxPlans = 32;
+
+struct DevGraph {
+  int32_t n_nodes;
+  int32_t n_edges;
+  int32_t rank_bits;
+  int32_t pad;
+  const int32_t *e_src;
+  const int32_t *e_dst;
+  const uint32_t *e_rank;
+  const int32_t *ptr[2];
+  const int32_t *nbr[2];
+  const uint32_t *rnk[2];
+  const uint64_t *pkey[2];
+  const int32_t *c2p[2];
+  const uint8_t *loop;
+};
+
+// per-column launch descriptor (device side)
+struct DevPlan {
+  int32_t family, endpoint, direction, exclude_trigger, cycle_len, min_size;
+  const uint32_t *lo_tab;  // rank -> first rank with time >= uniq_time[rank] - delta
+};
+
+struct DevPlans {
+  int32_t n;
+  int32_t needs_sets;  // any family beyond FAN/DEGREE/CYCLE_2
+  DevPlan p[kMaxPlans];
+};
+
+// ----------------------------------------------------------------- errors
+
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+void count_launch(int n = 1);
+
+#define TM_CUDA(expr)                                       \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return ::tmb::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define TM_LAUNCHED(name)                                   \
+  do {                                                      \
+    ::tmb::count_launch();                                   \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) return ::tmb::cuda_fail(_e, name); \
+  } while (0)
+
+// ----------------------------------------------------------------- memory
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  int ensure(size_t n);  // grow-only
+  template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// ----------------------------------------------------------------- sorting
+
+// Stable LSD radix sort of (key, value) pairs over key bits [0, nbits).
+// keys/vals hold the input; ktmp/vtmp are equally sized scratch.  On return
+// *kout/*vout point at whichever buffer holds the sorted result.
+int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n,
+                     int nbits, cudaStream_t s, uint64_t **kout, uint32_t **vout);
+
+// exclusive scan of uint32 counts (n <= 2^31) into out (may alias in)
+int exclusive_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, cudaStream_t s);
+
+inline int bits_for(uint64_t maxval) {  // bits to represent [0, maxval]
+  int b = 0;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+inline unsigned grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+}  // namespace tmb
+
+// ------------------------------------------------------------- the handle
+
+struct tm_graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool owns_stream = false;
+  int64_t n_nodes = 0, n_edges = 0, n_ranks = 0, n_selfloops = 0;
+  int64_t max_deg[2] = {0, 0};
+  int rank_bits = 0, node_bits = 0;
+  int64_t device_bytes = 0;
+
+  tmb::DevBuf e_src, e_dst, e_rank, uniq_time, loop;
+  tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], c2p[2];
+
+  // mining scratch (grow-only)
+  tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch;
+  int64_t lo_tab_cap = 0;
+  tm_mine_stats last{};
+  bool prof = false, prof_pending = false;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+
+  tmb::DevGraph dev() const;
+};

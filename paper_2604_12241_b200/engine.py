@@ -1,0 +1,168 @@
+"""`mine` — the drop-in replacement of tempmine.engine.mine (engine.py:658-712).
+
+Same signature, same column order (order_plans, engine.py:596-604), same
+errors (EngineInvariantError for duplicate names / slot mismatch, ValueError
+for workers < 1), same return type (FeatureMatrix, engine.py:55-103).  The
+work runs in libtempmine_b200.so on one GPU; `workers` is accepted for API
+compatibility (the reference's fork-pool width) and has no effect — the
+whole trigger range is one launch, balanced on the device.  Paths the GPU
+does not implement (members attribution, instance collection, arbitrary
+GENERIC stage programs) raise UnsupportedPlanError instead of silently
+falling back to a CPU interpreter.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .graph import DeviceGraph, as_device_graph
+from .plan import BUILTIN_COLUMNS, PlanDesc, lower_plan
+
+
+class EngineInvariantError(RuntimeError):
+    """engine.py:33"""
+
+
+@dataclass
+class FeatureMatrix:
+    """Per-edge pattern counts plus the edge identity columns (engine.py:55-103)."""
+
+    columns: tuple
+    values: np.ndarray  # (edge_count, len(columns)) int64
+    edge_src: np.ndarray
+    edge_dst: np.ndarray
+    edge_time: np.ndarray
+    edge_label: np.ndarray
+
+    @property
+    def edge_count(self) -> int:
+        return len(self.edge_src)
+
+    def column(self, name: str) -> np.ndarray:
+        return self.values[:, self.columns.index(name)]
+
+    def to_csv(self, path: str) -> None:
+        """edge_id,src,dst,timestamp,label,<features> — byte-identical to the
+        reference writer (engine.py:73-103): empty label cell when < 0."""
+        n = self.edge_count
+        with open(path, "w", encoding="utf-8", newline="\n") as fh:
+            fh.write("edge_id,src,dst,timestamp,label")
+            for col in self.columns:
+                fh.write("," + col)
+            fh.write("\n")
+            chunk = 65536
+            lab = np.asarray(self.edge_label).astype(np.int64)
+            for start in range(0, n, chunk):
+                stop = min(start + chunk, n)
+                ids = np.arange(start, stop, dtype=np.int64).astype(str)
+                cols = [ids, np.asarray(self.edge_src[start:stop], dtype=np.int64).astype(str),
+                        np.asarray(self.edge_dst[start:stop], dtype=np.int64).astype(str),
+                        np.asarray(self.edge_time[start:stop], dtype=np.int64).astype(str)]
+                lab_s = lab[start:stop].astype(str)
+                lab_s[lab[start:stop] < 0] = ""
+                cols.append(lab_s)
+                for j in range(len(self.columns)):
+                    cols.append(self.values[start:stop, j].astype(str))
+                rows = cols[0]
+                for c in cols[1:]:
+                    rows = np.char.add(np.char.add(rows, ","), c)
+                fh.write("\n".join(rows.tolist()))
+                fh.write("\n")
+
+
+def merge_features(partials: list) -> FeatureMatrix:
+    """engine.py:106-120 — elementwise integer sum."""
+    if not partials:
+        raise EngineInvariantError("nothing to merge")
+    first = partials[0]
+    total = first.values.copy()
+    for other in partials[1:]:
+        if tuple(other.columns) != tuple(first.columns):
+            raise EngineInvariantError(f"column mismatch in merge: {other.columns} vs {first.columns}")
+        if other.values.shape != first.values.shape:
+            raise EngineInvariantError("row-count mismatch in merge")
+        total += other.values
+    return FeatureMatrix(first.columns, total, first.edge_src, first.edge_dst, first.edge_time,
+                         first.edge_label)
+
+
+def order_plans(plans: list) -> list:
+    """engine.py:596-604 — builtin columns first in canonical order, then the
+    rest in the order given; duplicate names are an error."""
+    names = [p.name for p in plans]
+    if len(set(names)) != len(names):
+        raise EngineInvariantError(f"duplicate pattern names in {names}")
+    builtin = [p for name in BUILTIN_COLUMNS for p in plans if p.name == name]
+    custom = [p for p in plans if p.name not in BUILTIN_COLUMNS]
+    return builtin + custom
+
+
+def lower_all(plans: list) -> tuple[list, list[PlanDesc]]:
+    plans = order_plans(list(plans))
+    for p in plans:
+        if p.slot_count != len(p.cells):
+            raise EngineInvariantError(f"plan {p.name}: slot count disagrees with cells")
+    descs = [lower_plan(p) for p in plans]
+    if len(descs) > _lib.MAX_PLANS:
+        raise ValueError(f"at most {_lib.MAX_PLANS} columns per mine() call")
+    return plans, descs
+
+
+def mine_rows(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int,
+              out: np.ndarray | None = None) -> np.ndarray:
+    """Rows [lo, hi) x len(descs) into a host int64 array (C order)."""
+    rows = hi - lo
+    if out is None:
+        out = np.empty((rows, len(descs)), dtype=np.int64)
+    if rows == 0 or not descs:
+        return out
+    arr = _lib.plan_array(descs)
+    rc = _lib.load().tm_mine(dgraph.handle, arr, len(descs), lo, hi, _lib.ptr(out), 0, None)
+    _lib.check(rc, "tm_mine")
+    return out
+
+
+def mine_rows_device(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int, out_ptr: int,
+                     stream: int | None = None) -> None:
+    """Enqueue rows [lo, hi) into a device int64 buffer at out_ptr (row-major,
+    len(descs) columns) on `stream`; returns without synchronizing."""
+    if hi <= lo or not descs:
+        return
+    arr = _lib.plan_array(descs)
+    rc = _lib.load().tm_mine(dgraph.handle, arr, len(descs), lo, hi, ctypes.c_void_p(out_ptr), 1,
+                             ctypes.c_void_p(stream) if stream else None)
+    _lib.check(rc, "tm_mine")
+
+
+def last_stats(dgraph: DeviceGraph) -> _lib.TmMineStats:
+    st = _lib.TmMineStats()
+    _lib.check(_lib.load().tm_last_mine_stats(dgraph.handle, ctypes.byref(st)), "tm_last_mine_stats")
+    return st
+
+
+def mine(graph, plans, workers: int = 1, collect_instances: bool = False, *, device: int = 0):
+    """Mine every plan over every trigger edge on the GPU (engine.py:658).
+
+    `graph` is a DeviceGraph or any TemporalGraph-like object (edge_src,
+    edge_dst, edge_time, node_count); the latter is uploaded and built on the
+    device once and cached for the lifetime of the graph object.
+    """
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    if collect_instances:
+        raise _lib.UnsupportedPlanError(
+            _lib.TM_E_UNSUPPORTED_PLAN,
+            "collect_instances=True needs per-instance records, which the GPU path does not emit")
+    plans, descs = lower_all(plans)
+    dg = as_device_graph(graph, device)
+    values = mine_rows(dg, descs, 0, dg.edge_count)
+    label = getattr(graph, "edge_label", None)
+    if label is None:
+        label = dg.edge_label
+    return FeatureMatrix(columns=tuple(p.name for p in plans), values=values,
+                         edge_src=graph.edge_src, edge_dst=graph.edge_dst,
+                         edge_time=graph.edge_time, edge_label=label)

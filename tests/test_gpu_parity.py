@@ -1,0 +1,225 @@
+"""GPU parity: libtempmine_b200.so (via the C ABI) against the reference's
+recorded outputs (tests/golden) and against the pinned CPU oracle.
+
+Bar: bit-exact int64 equality for every column of every row.
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, columns_of, corpus_graphs, load_hand, load_npz
+from oracle.oracle import OracleGraph, column
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tmb():
+    import paper_2604_12241_b200 as tmb
+    tmb.build and None
+    from paper_2604_12241_b200 import build
+    build.build()
+    return tmb
+
+
+def _descs(tmb, cols, delta):
+    return [tmb.lower_plan(tmb.builtin_plan(c["base"], delta, c["min_size"], column=c["column"]))
+            for c in cols]
+
+
+def _mine(tmb, src, dst, t, cols, delta, node_count=None):
+    g = tmb.DeviceGraph(src, dst, t, node_count=node_count)
+    out = tmb.mine_rows(g, _descs(tmb, cols, delta), 0, g.edge_count)
+    g.free()
+    return out
+
+
+def _split(tmb, cols):
+    # at most 32 columns per launch
+    return [cols[i:i + 32] for i in range(0, len(cols), 32)]
+
+
+def test_hand_cases(tmb):
+    doc = load_hand()
+    for case in doc["cases"]:
+        e = np.array(case["edges"], dtype=np.int64)
+        got = _mine(tmb, e[:, 0], e[:, 1], e[:, 2], doc["columns"], case["delta"])
+        np.testing.assert_array_equal(got, np.array(case["values"]), err_msg=f"{case['name']} d={case['delta']}")
+
+
+def test_acceptance_corpus(tmb):
+    z = load_npz("corpus.npz")
+    cols = columns_of(z)
+    n = 0
+    for i, edges, deltas, vals in corpus_graphs():
+        g = tmb.DeviceGraph(edges[:, 0], edges[:, 1], edges[:, 2])
+        for k, d in enumerate(deltas.tolist()):
+            got = tmb.mine_rows(g, _descs(tmb, cols, d), 0, g.edge_count)
+            np.testing.assert_array_equal(got, vals[:, k, :], err_msg=f"graph {i} delta {d}")
+            n += 1
+        g.free()
+    assert n == 600
+
+
+@pytest.mark.skipif(not (GOLDEN / "ties.npz").exists(), reason="fixture not generated")
+def test_ties_and_selfloops(tmb):
+    z = load_npz("ties.npz")
+    cols = columns_of(z)
+    meta = json.loads(str(z["meta"]))
+    for idx, m in enumerate(meta):
+        g = tmb.DeviceGraph(z[f"src{idx}"], z[f"dst{idx}"], z[f"time{idx}"])
+        for k, d in enumerate(m["deltas"]):
+            got = tmb.mine_rows(g, _descs(tmb, cols, d), 0, g.edge_count)
+            np.testing.assert_array_equal(got, z[f"values{idx}"][:, k, :], err_msg=f"ties {idx} delta {d}")
+        g.free()
+
+
+@pytest.mark.skipif(not (GOLDEN / "cfg1.npz").exists(), reason="fixture not generated")
+def test_cfg1_reference_output(tmb):
+    """cfg1: 102K edges, alpha = 2.1 giant hub — exercises the
+    heavy (warp) queue; every column equals the reference's."""
+    from paper_2604_12241_b200 import synth
+    z = load_npz("cfg1.npz")
+    g0 = synth.generate(synth.CONFIGS["cfg1"])
+    cols = columns_of(z)
+    got = _mine(tmb, g0.src, g0.dst, g0.time, cols, 86400)
+    np.testing.assert_array_equal(got, z["values"])
+
+
+def test_csr_matches_reference_layout(tmb):
+    rng = np.random.default_rng(3)
+    n, e = 300, 20000
+    src = rng.integers(0, n, e)
+    dst = rng.integers(0, n, e)
+    t = rng.integers(0, 50, e) * 1000 + 10**12  # ties + large absolute times
+    g = tmb.DeviceGraph(src, dst, t, node_count=n + 5)
+    eids = np.arange(e)
+    for direction, owner, other in (("out", src, dst), ("in", dst, src)):
+        indptr, nbr, tim, eid = g.export_csr(direction)
+        order = np.lexsort((eids, t, owner))  # txgraph.py:135-136
+        np.testing.assert_array_equal(eid, order)
+        np.testing.assert_array_equal(nbr, other[order])
+        np.testing.assert_array_equal(tim, t[order])
+        np.testing.assert_array_equal(indptr, np.concatenate([[0], np.cumsum(np.bincount(owner, minlength=n + 5))]))
+    info = g.info()
+    assert info.n_ranks == len(np.unique(t))
+    st = g.stats
+    assert st.mean_out_degree == pytest.approx(e / (n + 5))
+
+
+ALL = ["fan_in", "fan_out", "deg_in_src", "deg_out_src", "deg_in_dst", "deg_out_dst", "cycle_2",
+       "cycle_3", "cycle_4", "cycle_5", "cycle_6", "cycle_7", "cycle_8", "sg_count", "gs_count",
+       "stack_count"]
+
+
+def _oracle_vs_gpu(tmb, src, dst, t, delta, names=ALL, ks=None, rows=None):
+    og = OracleGraph(src, dst, t)
+    ks = ks or [None] * len(names)
+    want = og.mine([column(nm, delta, k) for nm, k in zip(names, ks)])
+    g = tmb.DeviceGraph(src, dst, t)
+    descs = [tmb.lower_plan(tmb.builtin_plan(nm, delta, k)) for nm, k in zip(names, ks)]
+    got = tmb.mine_rows(g, descs, 0, g.edge_count)
+    st = tmb.last_stats(g)
+    g.free()
+    for j, nm in enumerate(names):
+        bad = np.flatnonzero(got[:, j] != want[:, j])
+        assert len(bad) == 0, f"{nm}: {len(bad)} rows differ, e.g. row {bad[:5]} got {got[bad[:5], j]} want {want[bad[:5], j]}"
+    return st
+
+
+def test_powerlaw_hubs_vs_oracle(tmb):
+    """alpha = 1.0 / 2.1 hubs, parallel edges, many heavy triggers."""
+    from paper_2604_12241_b200 import synth
+    for alpha, n, m in ((2.1, 3000, 60000), (1.0, 20000, 200000)):
+        cfg = synth.SynthConfig(n, m, 8 * 86400, seed=11, powerlaw_exponent=alpha,
+                                plants=(synth.PlantSpec("sg_count", 40), synth.PlantSpec("cycle_4", 40)))
+        g0 = synth.generate(cfg)
+        st = _oracle_vs_gpu(tmb, g0.src, g0.dst, g0.time, 86400)
+        assert st.heavy_triggers > 0  # the warp path was exercised
+
+
+def test_dense_small_graph_vs_oracle(tmb):
+    """Dense windows: long cycle chains, large intersections, self-loops."""
+    rng = np.random.default_rng(21)
+    n, e = 60, 6000
+    src = rng.integers(0, n, e)
+    dst = rng.integers(0, n, e)
+    t = rng.integers(0, 400, e)
+    _oracle_vs_gpu(tmb, src, dst, t, 25)
+    _oracle_vs_gpu(tmb, src, dst, t, 0)
+    _oracle_vs_gpu(tmb, src, dst, t, 3, names=["sg_count", "gs_count", "cycle_4", "cycle_5", "stack_count"],
+                   ks=[1, 3, 2, 2, 3])
+
+
+def test_window_monotone_in_delta(tmb):
+    """Property (test_acceptance.py:244-261): every count is non-decreasing in
+    delta for the unthresholded columns."""
+    from paper_2604_12241_b200 import synth
+    g0 = synth.generate(synth.SynthConfig(5000, 80000, 30 * 86400, seed=3, powerlaw_exponent=1.2))
+    g = tmb.DeviceGraph(g0.src, g0.dst, g0.time)
+    names = ["fan_in", "fan_out", "deg_in_src", "deg_out_dst", "cycle_2", "cycle_3", "cycle_4", "stack_count"]
+    prev = None
+    for d in (0, 600, 3600, 86400, 7 * 86400):
+        cur = tmb.mine_rows(g, [tmb.lower_plan(tmb.builtin_plan(nm, d, 1)) for nm in names], 0, g.edge_count)
+        if prev is not None:
+            assert (cur >= prev).all()
+        prev = cur
+    g.free()
+
+
+def test_ranges_and_determinism(tmb):
+    rng = np.random.default_rng(8)
+    src = rng.integers(0, 500, 30000)
+    dst = rng.integers(0, 500, 30000)
+    t = rng.integers(0, 10000, 30000)
+    g = tmb.DeviceGraph(src, dst, t)
+    descs = [tmb.lower_plan(p) for p in tmb.full_pattern_set(300)]
+    full = tmb.mine_rows(g, descs, 0, g.edge_count)
+    again = tmb.mine_rows(g, descs, 0, g.edge_count)
+    np.testing.assert_array_equal(full, again)
+    np.testing.assert_array_equal(tmb.mine_rows(g, descs, 1234, 20000), full[1234:20000])
+    assert tmb.mine_rows(g, descs, 5, 5).shape == (0, 14)
+    g.free()
+
+
+def test_mine_api_drop_in(tmb):
+    """mine(graph, plans) with a TemporalGraph-like host object: FeatureMatrix,
+    column order per order_plans (engine.py:596-604), errors as the reference."""
+    from types import SimpleNamespace
+    e = np.array([(0, 2, 1), (0, 3, 2), (0, 4, 3), (2, 1, 4), (3, 1, 5), (4, 1, 6)], dtype=np.int64)
+    g = SimpleNamespace(node_count=5, edge_src=e[:, 0], edge_dst=e[:, 1], edge_time=e[:, 2],
+                        edge_label=np.full(6, -1, np.int8))
+    plans = [tmb.builtin_plan("gs_count", 10), tmb.builtin_plan("sg_count", 10), tmb.builtin_plan("fan_in", 10)]
+    fm = tmb.mine(g, plans, workers=4)
+    assert fm.columns == ("fan_in", "sg_count", "gs_count")
+    assert fm.column("sg_count").tolist() == [0, 0, 0, 0, 1, 1]
+    assert fm.values.dtype == np.int64
+    with pytest.raises(ValueError):
+        tmb.mine(g, plans, workers=0)
+    with pytest.raises(tmb.EngineInvariantError):
+        tmb.mine(g, plans + [tmb.builtin_plan("fan_in", 3)])
+    with pytest.raises(tmb.UnsupportedPlanError):
+        tmb.mine(g, plans, collect_instances=True)
+
+
+def test_bad_graphs_raise(tmb):
+    with pytest.raises(ValueError):
+        tmb.DeviceGraph([0, 5], [1, 1], [0, 0], node_count=3)  # id outside [0, n)
+    g = tmb.DeviceGraph([0], [1], [7])
+    assert tmb.mine_rows(g, [tmb.lower_plan(tmb.builtin_plan("deg_out_src", 5))], 0, 1).tolist() == [[1]]
+    with pytest.raises(ValueError):
+        tmb.mine_rows(g, [tmb.lower_plan(tmb.builtin_plan("fan_in", 5))], 0, 2)
+    g.free()
+
+
+def test_single_timestamp_and_extreme_times(tmb):
+    src = np.array([0, 1, 2, 0, 1], dtype=np.int64)
+    dst = np.array([1, 2, 0, 2, 0], dtype=np.int64)
+    for t0 in (0, 2**62, -(2**40)):
+        t = np.full(5, t0, dtype=np.int64)
+        _oracle_vs_gpu(tmb, src, dst, t, 0)
+        _oracle_vs_gpu(tmb, src, dst, t, 2**61)
