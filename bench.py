@@ -221,7 +221,11 @@ def main():
     log(f"[bench] rank {rank}: graph built in {build_s:.2f}s, {info.device_bytes / 2**30:.2f} GiB, "
         f"max out/in degree {info.max_out_degree}/{info.max_in_degree}, rows [{lo},{hi})")
 
-    stream = torch.cuda.current_stream()
+    # a non-default stream: its handle is non-NULL, so the library launches on
+    # it (NULL would select the graph's own stream) and the events below see
+    # exactly the mining kernels' stream
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     out_local = torch.empty((chunk, C), dtype=torch.int64, device="cuda")
     out_full = torch.empty((chunk * world, C), dtype=torch.int64, device="cuda") if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

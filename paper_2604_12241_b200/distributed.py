@@ -68,10 +68,15 @@ def mine_distributed(graph, plans, *, group=None):
 
     plans, descs = lower_all(plans)
     dg = as_device_graph(graph, torch.cuda.current_device())
-    stream = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
 
     def block(lo, hi, out):
-        mine_rows_device(dg, descs, lo, hi, out.data_ptr(), stream.cuda_stream)
+        # launch on a non-NULL stream (NULL selects the graph's own stream),
+        # then order the all-gather on the current stream after it
+        side.wait_stream(torch.cuda.current_stream())
+        out.record_stream(side)
+        mine_rows_device(dg, descs, lo, hi, out.data_ptr(), side.cuda_stream)
+        torch.cuda.current_stream().wait_stream(side)
 
     full = mine_sharded(dg.edge_count, len(descs), dist.get_rank(group), dist.get_world_size(group),
                         block, device="cuda", group=group)

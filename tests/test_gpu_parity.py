@@ -20,9 +20,8 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(scope="module")
 def tmb():
     import paper_2604_12241_b200 as tmb
-    tmb.build and None
-    from paper_2604_12241_b200 import build
-    build.build()
+    from paper_2604_12241_b200 import _lib
+    _lib.load()  # the in-tree .so; raises (no fallback) if it is missing
     return tmb
 
 
