@@ -136,7 +136,7 @@ struct tm_graph {
   tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], c2p[2];
 
   // mining scratch (grow-only)
-  tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch;
+  tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks;
   int64_t lo_tab_cap = 0;
   tm_mine_stats last{};
   bool prof = false, prof_pending = false;
