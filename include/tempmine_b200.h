@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define TM_ABI_VERSION 1
+#define TM_ABI_VERSION 2
 
 /* pattern families (plan.py kernel hints + the extended north-star set) */
 enum tm_family {
@@ -95,7 +95,11 @@ typedef struct tm_mine_stats {
   int64_t kernel_launches;/* launches issued by the last tm_mine */
   float light_ms;         /* CUDA-event time of the last call's per-thread
                              kernel (profiling on), else -1 */
-  float heavy_ms;         /* same for the per-warp heavy kernel */
+  float heavy_ms;         /* same for the heavy (per-warp + task) kernels,
+                             summed over pipeline chunks (they overlap the
+                             next chunk's light kernel) */
+  float total_ms;         /* CUDA-event time of the whole call on the device */
+  int32_t reserved;
 } tm_mine_stats;
 
 int tm_abi_version(void);

@@ -45,7 +45,8 @@ class TmGraphInfo(ctypes.Structure):
 class TmMineStats(ctypes.Structure):
     _fields_ = [("triggers", ctypes.c_int64), ("heavy_triggers", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("light_ms", ctypes.c_float),
-                ("heavy_ms", ctypes.c_float)]
+                ("heavy_ms", ctypes.c_float), ("total_ms", ctypes.c_float),
+                ("reserved", ctypes.c_int32)]
 
 
 # name -> (restype, argtypes): every symbol include/tempmine_b200.h declares
@@ -66,7 +67,7 @@ SIGNATURES = {
     "tm_last_error": (ctypes.c_char_p, []),
     "tm_graph_free": (None, [_P]),
 }
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class TempmineError(RuntimeError):
@@ -91,7 +92,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        p = Path(path) if path else Path(os.environ.get("TM_LIB", LIB_PATH))
         if not p.exists():
             raise RuntimeError(
                 f"{p} is missing: build it with `python -m paper_2604_12241_b200.build` "

@@ -36,14 +36,15 @@ def needs_build() -> bool:
     return any(d.stat().st_mtime > mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Compile the library; `defines` (e.g. ["TM_SMALL_RUN=0"]) and `out` build tuning variants."""
+    if not force and not needs_build() and not defines and out is None:
         return LIB
-    objdir = HERE / "build"
-    objdir.mkdir(exist_ok=True)
+    objdir = HERE / "build" / ("_".join(d.replace("=", "") for d in defines) or "default")
+    objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-             "--expt-relaxed-constexpr", *ARCH]
+             "--expt-relaxed-constexpr", *ARCH, *[f"-D{d}" for d in defines]]
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
         cmd = [nvcc(), "-c", str(CSRC / src), "-o", str(obj), *flags]
@@ -53,13 +54,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose and res.stderr:
             print(res.stderr, file=sys.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    target = out or LIB
+    tmp = target.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-o", str(tmp), *objs, *ARCH, "-cudart", "static"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -119,14 +119,18 @@ __global__ void k_indptr(const uint64_t *__restrict__ keys, int64_t n, int shift
   for (int64_t x = prev + 1; x <= cur; ++x) ptr[x] = (int32_t)p;
 }
 
-__global__ void k_pair_fill(const uint32_t *__restrict__ pids, const int32_t *__restrict__ nbr,
-                            const uint32_t *__restrict__ rnk, int64_t n, int rbits,
-                            uint64_t *__restrict__ pkey, int32_t *__restrict__ c2p) {
+// pair slot q holds CSR slot p = pids[q]; runs of equal (owner, nbr) are in
+// time order, so the pair predecessor is the previous occurrence of the same
+// neighbour: prev[p] = its rank + 1 (0 = none)
+__global__ void k_pair_fill(const uint64_t *__restrict__ pair_sorted, const uint32_t *__restrict__ pids,
+                            const int32_t *__restrict__ nbr, const uint32_t *__restrict__ rnk,
+                            int64_t n, int rbits, uint64_t *__restrict__ pkey,
+                            uint32_t *__restrict__ prev) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const uint32_t p = pids[q];
   pkey[q] = ((uint64_t)(uint32_t)nbr[p] << rbits) | rnk[p];
-  c2p[p] = (int32_t)q;
+  prev[p] = (q > 0 && pair_sorted[q - 1] == pair_sorted[q]) ? rnk[pids[q - 1]] + 1u : 0u;
 }
 
 __global__ void k_max_degree(const int32_t *__restrict__ ptr, int64_t n_nodes,
@@ -177,7 +181,7 @@ tmb::DevGraph tm_graph::dev() const {
     g.nbr[d] = nbr[d].as<int32_t>();
     g.rnk[d] = rnk[d].as<uint32_t>();
     g.pkey[d] = pkey[d].as<uint64_t>();
-    g.c2p[d] = c2p[d].as<int32_t>();
+    g.prev[d] = prev[d].as<uint32_t>();
   }
   g.loop = loop.as<uint8_t>();
   return g;
@@ -212,7 +216,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
   for (int d = 0; d < 2; ++d) {
     if ((rc = g->ptr[d].ensure(4 * (N + 1))) || (rc = g->nbr[d].ensure(4 * Ea)) ||
         (rc = g->rnk[d].ensure(4 * Ea)) || (rc = g->eid[d].ensure(4 * Ea)) ||
-        (rc = g->pkey[d].ensure(8 * Ea)) || (rc = g->c2p[d].ensure(4 * Ea)))
+        (rc = g->pkey[d].ensure(8 * Ea)) || (rc = g->prev[d].ensure(4 * Ea)))
       return rc;
   }
   if (E == 0) {
@@ -305,9 +309,9 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
     uint64_t *pk2 = (pk == ka.as<uint64_t>()) ? kb.as<uint64_t>() : ka.as<uint64_t>();
     uint32_t *pv2 = (pv == va.as<uint32_t>()) ? vb.as<uint32_t>() : va.as<uint32_t>();
     if ((rc = radix_sort_pairs(pk, pv, pk2, pv2, E, 2 * g->node_bits, s, &ps, &pvs))) return rc;
-    k_pair_fill<<<grid_for(E, kB), kB, 0, s>>>(pvs, g->nbr[d].as<int32_t>(), g->rnk[d].as<uint32_t>(),
-                                               E, g->rank_bits, g->pkey[d].as<uint64_t>(),
-                                               g->c2p[d].as<int32_t>());
+    k_pair_fill<<<grid_for(E, kB), kB, 0, s>>>(ps, pvs, g->nbr[d].as<int32_t>(),
+                                               g->rnk[d].as<uint32_t>(), E, g->rank_bits,
+                                               g->pkey[d].as<uint64_t>(), g->prev[d].as<uint32_t>());
     TM_LAUNCHED("k_pair_fill");
     unsigned long long *md = reinterpret_cast<unsigned long long *>(st.p);
     TM_CUDA(cudaMemsetAsync(md, 0, 8, s));
@@ -358,7 +362,7 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
   for (const DevBuf *b : {&g->e_src, &g->e_dst, &g->e_rank, &g->uniq_time, &g->loop})
     bytes += (int64_t)b->bytes;
   for (int d = 0; d < 2; ++d)
-    for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->c2p[d]})
+    for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d]})
       bytes += (int64_t)b->bytes;
   g->device_bytes = bytes;
   *out = g;
@@ -436,6 +440,15 @@ extern "C" void tm_graph_free(tm_graph *g) {
   cudaStream_t s = g->stream;
   for (int i = 0; i < 3; ++i)
     if (g->ev[i]) cudaEventDestroy(g->ev[i]);
+  for (int c = 0; c < kMaxChunks; ++c)
+    for (int i = 0; i < 4; ++i)
+      if (g->pev[c][i]) cudaEventDestroy(g->pev[c][i]);
+  if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+  if (g->ev_join) cudaEventDestroy(g->ev_join);
+  if (g->side) {
+    cudaStreamSynchronize(g->side);
+    cudaStreamDestroy(g->side);
+  }
   delete g;  // DevBuf destructors free device memory
   if (own && s) cudaStreamDestroy(s);
 }

@@ -13,12 +13,14 @@
 //                    np.lexsort((eid, time, owner)) (txgraph.py:134-144):
 //                    nbr int32[E], rnk uint32[E], eid int32[E]
 //   pair index       same runs re-sorted by (owner, nbr, rank, eid):
-//                    pkey uint64[E] = nbr << rank_bits | rank; c2p int32[E]
-//                    maps a CSR position to its pair position.  It answers
-//                    "edge a->b inside the window?" with one bisection and
-//                    "is CSR entry j the first occurrence of its neighbour in
-//                    the window?" (np.unique dedup, kernels.py:59) with one
-//                    load of the pair predecessor.
+//                    pkey uint64[E] = nbr << rank_bits | rank — answers "edge
+//                    a->b inside the window?" by bisection when both windows
+//                    are wide.
+//   previous occurrence  prev uint32[E] per CSR slot: rank + 1 of the
+//                    previous entry with the same (owner, nbr), 0 = none.
+//                    Entry j is the first occurrence of its neighbour inside
+//                    the window [lo, hi] (np.unique dedup, kernels.py:59)
+//                    iff prev[j] <= lo: one coalesced load along the window.
 //   self-loop flags  loop uint8[N] (txgraph.py:146-153 self-loop CSR)
 #pragma once
 
@@ -33,6 +35,7 @@
 namespace tmb {
 
 constexpr int kMaxPlans = 32;
+constexpr int kMaxChunks = 4;  // tm_mine pipeline depth
 
 struct DevGraph {
   int32_t n_nodes;
@@ -46,14 +49,28 @@ struct DevGraph {
   const int32_t *nbr[2];
   const uint32_t *rnk[2];
   const uint64_t *pkey[2];
-  const int32_t *c2p[2];
+  const uint32_t *prev[2];
   const uint8_t *loop;
+};
+
+// fused cycle enumeration shared by the CYCLE columns (length 3..8) of one
+// delta; depth d <-> cycle length d + 3
+struct CycGroup {
+  int32_t mask;    // bit d: some column wants cycle length d + 3
+  int32_t maxd;    // deepest chain (0..5)
+  int32_t lead;    // this column runs the enumeration and writes all members
+  int32_t k[6];    // min_size per depth
+  int8_t col[6];   // output column per depth
+  int8_t pad[2];
 };
 
 // per-column launch descriptor (device side)
 struct DevPlan {
   int32_t family, endpoint, direction, exclude_trigger, cycle_len, min_size;
+  int32_t need;        // trigger windows this column reads (1 u-in, 2 u-out, 4 v-in, 8 v-out)
+  int32_t need_group;  // union over the columns sharing this delta
   const uint32_t *lo_tab;  // rank -> first rank with time >= uniq_time[rank] - delta
+  CycGroup cyc;            // CYCLE with cycle_len >= 3 only
 };
 
 struct DevPlans {
@@ -133,14 +150,19 @@ struct tm_graph {
   int64_t device_bytes = 0;
 
   tmb::DevBuf e_src, e_dst, e_rank, uniq_time, loop;
-  tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], c2p[2];
+  tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2];
 
   // mining scratch (grow-only)
   tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks;
   int64_t lo_tab_cap = 0;
   tm_mine_stats last{};
   bool prof = false, prof_pending = false;
+  int prof_chunks = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // chunk pipeline: side stream for the heavy tier, per-chunk events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t pev[tmb::kMaxChunks][4] = {};
 
   tmb::DevGraph dev() const;
 };
