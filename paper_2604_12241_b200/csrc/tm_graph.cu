@@ -440,15 +440,7 @@ extern "C" void tm_graph_free(tm_graph *g) {
   cudaStream_t s = g->stream;
   for (int i = 0; i < 3; ++i)
     if (g->ev[i]) cudaEventDestroy(g->ev[i]);
-  for (int c = 0; c < kMaxChunks; ++c)
-    for (int i = 0; i < 4; ++i)
-      if (g->pev[c][i]) cudaEventDestroy(g->pev[c][i]);
-  if (g->ev_fork) cudaEventDestroy(g->ev_fork);
-  if (g->ev_join) cudaEventDestroy(g->ev_join);
-  if (g->side) {
-    cudaStreamSynchronize(g->side);
-    cudaStreamDestroy(g->side);
-  }
+
   delete g;  // DevBuf destructors free device memory
   if (own && s) cudaStreamDestroy(s);
 }

@@ -35,7 +35,6 @@
 namespace tmb {
 
 constexpr int kMaxPlans = 32;
-constexpr int kMaxChunks = 4;  // tm_mine pipeline depth
 
 struct DevGraph {
   int32_t n_nodes;
@@ -53,30 +52,46 @@ struct DevGraph {
   const uint8_t *loop;
 };
 
-// fused cycle enumeration shared by the CYCLE columns (length 3..8) of one
-// delta; depth d <-> cycle length d + 3
-struct CycGroup {
-  int32_t mask;    // bit d: some column wants cycle length d + 3
-  int32_t maxd;    // deepest chain (0..5)
-  int32_t lead;    // this column runs the enumeration and writes all members
-  int32_t k[6];    // min_size per depth
-  int8_t col[6];   // output column per depth
-  int8_t pad[2];
-};
+constexpr int kMaxChain = 5;   // cycle_8: chain a1..a5
+constexpr int kMaxCyc = 6;     // cycle_3..8 columns per group (more: another group, same delta)
+constexpr int kMaxGroups = 8;  // distinct deltas per tm_mine call
 
 // per-column launch descriptor (device side)
 struct DevPlan {
   int32_t family, endpoint, direction, exclude_trigger, cycle_len, min_size;
-  int32_t need;        // trigger windows this column reads (1 u-in, 2 u-out, 4 v-in, 8 v-out)
-  int32_t need_group;  // union over the columns sharing this delta
+  int32_t group;  // delta group
+};
+
+// one fused chain enumeration for every cycle_3..8 column of a delta group;
+// entry e closes at chain depth depth[e] (cycle length depth + 3)
+struct CycGroup {
+  int32_t mask;  // bit d: some column closes at depth d
+  int32_t maxd;  // deepest chain (0..5)
+  int32_t n;     // entries
+  int32_t k[kMaxCyc];      // min_size per entry
+  int8_t depth[kMaxCyc];
+  int8_t col[kMaxCyc];     // output column per entry
+};
+
+// the columns sharing one delta: one set of trigger windows, one
+// lower-bound table, one pass over each trigger slice
+struct DevGroup {
   const uint32_t *lo_tab;  // rank -> first rank with time >= uniq_time[rank] - delta
-  CycGroup cyc;            // CYCLE with cycle_len >= 3 only
+  int32_t need;            // trigger windows (1 u-in, 2 u-out, 4 v-in, 8 v-out)
+  int32_t udom, vdom;      // N-(u) / N+(v) item passes needed
+  int32_t has_stack;
+  int32_t ncols, n_sg, n_gs;
+  int8_t cols[kMaxPlans];
+  int8_t sg_col[kMaxPlans];
+  int8_t gs_col[kMaxPlans];
+  CycGroup cyc;
 };
 
 struct DevPlans {
   int32_t n;
-  int32_t needs_sets;  // any family beyond FAN/DEGREE/CYCLE_2
+  int32_t ngroups;
   DevPlan p[kMaxPlans];
+  DevGroup gr[kMaxGroups];
 };
 
 // ----------------------------------------------------------------- errors
@@ -153,16 +168,11 @@ struct tm_graph {
   tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2];
 
   // mining scratch (grow-only)
-  tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks;
+  tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks, split_scratch;
   int64_t lo_tab_cap = 0;
   tm_mine_stats last{};
   bool prof = false, prof_pending = false;
-  int prof_chunks = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-  // chunk pipeline: side stream for the heavy tier, per-chunk events
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaEvent_t pev[tmb::kMaxChunks][4] = {};
 
   tmb::DevGraph dev() const;
 };

@@ -10,48 +10,49 @@
 //                    Appendix B (per-binding set_cardinality :462-464,
 //                    source_count :483-485)
 //
-// Work balancing for power-law hubs (the reference has none: equal
-// contiguous ranges per worker, engine.py:681-682) — three tiers:
+// Work decomposition (the reference splits contiguous trigger ranges per
+// worker, engine.py:681-682, and walks each trigger serially):
 //
-//   k_mine_light   one THREAD per trigger edge, all columns.  The trigger's
-//                  four windows are bisected once per delta group; set
-//                  columns iterate the SMALLER windowed slice and test the
-//                  other side with one pair-index bisection; distinct-ness is
-//                  an O(1) pair-predecessor test.  Each trigger carries a
-//                  work budget; a trigger that would exceed it is appended to
-//                  the heavy queue (warp-aggregated atomic) and left to ...
-//   k_mine_heavy   one WARP per heavy trigger: each column's outer slice is
-//                  spread over the lanes.  Outer slices longer than
-//                  kOuterSplit, and — inside cycle_k's depth-first chain
-//                  enumeration — every node whose windowed out-slice is
-//                  longer than kDeepSplit, are not walked serially but cut
-//                  into range TASKS of kTaskSpan entries, appended to a task
-//                  queue and ...
-//   k_mine_tasks   one WARP per task, lane per slice entry, launched in
-//                  rounds (a task only spawns tasks deeper in the chain, so
-//                  <= 5 rounds for cycle_8).  Partial counts are combined
-//                  with atomicAdd on the int64 output cell, which the heavy
-//                  kernel initialized with its own partial.
+// Every set column of a trigger e = (u -> v) is a sum over the distinct
+// neighbours of one of two windowed slices of e:
+//   U items  m in N-(u) \ {u, v}:  stack's a, cycle_3 (m in N+(v)),
+//            sg (|N+(m) ∩ N-(v)| >= K)
+//   V items  m in N+(v) \ {u, v}:  stack's c, gs (|N-(m) ∩ N+(u)| >= K),
+//            cycle_4..8 (chains a1 = m -> a2 -> ... closing into N-(u))
+//
+//   k_mine_warp    one warp = 32 triggers.  Each lane bisects its trigger's
+//                  four windows and computes FAN / DEGREE / cycle_2.  The
+//                  warp then FLATTENS the U items of all 32 triggers into one
+//                  list and deals it round-robin to its lanes (exclusive scan
+//                  of the slice lengths + a 5-step search of the owner), then
+//                  the V items — so a lane's cost no longer depends on its own
+//                  trigger's hub degree.  Item contributions go to the staged
+//                  output rows in shared memory with atomics; rows leave in
+//                  one coalesced write.
+//   task queue     a trigger slice longer than kDomSplit is not walked by the
+//                  warp but emitted as DOMAIN tasks of kTaskSpan entries; a
+//                  chain node whose out-window is longer than kDeepSplit is
+//                  emitted as a CHAIN task.  k_mine_tasks (one warp per task,
+//                  lane per entry) runs them in rounds — a task only spawns
+//                  deeper chain tasks — adding partial counts to the int64
+//                  output with atomicAdd.  stack's a * c and cycle_3's
+//                  threshold need the whole count: split rows keep a, c and
+//                  the raw cycle_3 count in a scratch slot that
+//                  k_mine_finalize turns into the column values.
 // Every count is an integer sum over disjoint pieces, so the result is
 // exactly the reference's regardless of the split.
-//
-// The chain enumeration is a compile-time-depth template (chain_level<CHAIN,
-// L>) so the path and loop state stay in registers; kernel parameters are
-// __grid_constant__ so taking their address does not spill them to local
-// memory.
 #include "tm_internal.cuh"
 
 namespace tmb {
 namespace {
 
-constexpr int kLightThreads = 128;
-constexpr int kHeavyThreads = 256;
-constexpr int kLightBudget = 96;   // default slice entries + probes per light trigger
-constexpr int kOuterSplit = 512;   // heavy row: outer slices above this become tasks
-constexpr int kDeepSplit = 64;     // chain nodes with wider windows become tasks
-constexpr int kTaskSpan = 128;     // entries per task (4 per lane)
-constexpr int kMaxChain = 5;       // cycle_8: a1..a5
-constexpr int kStageCols = 16;     // light rows staged in smem up to this many columns
+constexpr int kThreads = 128;        // k_mine_warp block (4 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr int kTaskThreads = 256;
+constexpr int kDomSplit = 256;       // a trigger slice above this becomes domain tasks
+constexpr int kDeepSplit = 64;       // chain nodes with wider windows become chain tasks
+constexpr int kTaskSpan = 128;       // entries per task (4 per lane)
+constexpr int kLvlDomU = 8, kLvlDomV = 9;  // Task::level of domain tasks
 
 struct Win {
   int a, b;
@@ -84,39 +85,19 @@ struct Ctx {
   const DevGraph &g;  // a __grid_constant__ kernel parameter
   int u, v;
   uint32_t lo, hi;    // window in rank space
-  Win wui, wuo, wvi, wvo;  // trigger windows, see fill_windows
+  Win wui, wuo, wvi, wvo;  // trigger windows (u-in, u-out, v-in, v-out)
 };
 
-// windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276).
-// Runs of <= kSmallRun entries (most accounts) are read with independent
-// loads and counted in registers — one memory round trip instead of two
-// dependent bisections; longer runs bisect.
-#ifndef TM_SMALL_RUN  // 0: always bisect (measured faster, see profiles/)
-#define TM_SMALL_RUN 0
-#endif
-constexpr int kSmallRun = TM_SMALL_RUN;
+// windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
 __device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
   const int a = __ldg(c.g.ptr[dir] + x), b = __ldg(c.g.ptr[dir] + x + 1);
-  const uint32_t *r = c.g.rnk[dir];
-  if (kSmallRun > 0 && b - a <= kSmallRun) {
-    int below = 0, upto = 0;
-#pragma unroll
-    for (int i = 0; i < kSmallRun; ++i) {
-      if (a + i < b) {
-        const uint32_t t = __ldg(r + a + i);
-        below += t < c.lo;
-        upto += t <= c.hi;
-      }
-    }
-    return {a + below, a + upto};
-  }
-  const int wa = lb_u32(r, a, b, c.lo);
-  return {wa, ub_u32(r, wa, b, c.hi)};
+  const int wa = lb_u32(c.g.rnk[dir], a, b, c.lo);
+  return {wa, ub_u32(c.g.rnk[dir], wa, b, c.hi)};
 }
 
-// the trigger-endpoint windows a plan group needs (DevPlan::need bits:
-// 1 u-in, 2 u-out, 4 v-in, 8 v-out) — bisected once per trigger and delta
+// trigger windows a delta group needs (bits: 1 u-in, 2 u-out, 4 v-in, 8 v-out)
 __device__ __forceinline__ void fill_windows(Ctx &c, int need) {
+  c.wui = c.wuo = c.wvi = c.wvo = Win{0, 0};
   if (need & 1) c.wui = window(c, 0, c.u);
   if (need & 2) c.wuo = window(c, 1, c.u);
   if (need & 4) c.wvi = window(c, 0, c.v);
@@ -139,11 +120,8 @@ __device__ __forceinline__ bool first_in_window(const Ctx &c, int dir, int j) {
 }
 
 // does x's dir-window w contain neighbour n?  Windows are time-local and
-// short: scan them; fall back to a pair-run bisection when w is wide.
-#ifndef TM_SCAN_WIN
-#define TM_SCAN_WIN 16
-#endif
-constexpr int kScanWin = TM_SCAN_WIN;
+// short: scan them; bisect the pair run when w is wide.
+constexpr int kScanWin = 16;
 __device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
   if (w.len() <= kScanWin) {
     bool hit = false;
@@ -162,137 +140,77 @@ __device__ __forceinline__ long long warp_sum(long long x) {
   return x;
 }
 
-// budget of the light (thread-per-trigger) tier; unlimited elsewhere
-struct Budget {
-  int left;
-  bool blown;
-  __device__ __forceinline__ bool take(int n) {
-    if (n > left) { blown = true; return false; }
-    left -= n;
-    return true;
-  }
-};
-
 // ------------------------------------------------------------ task queue
 
 struct Task {
   int32_t row;   // trigger row (relative to lo); < 0 = empty slot
-  int8_t col;    // plan index
-  int8_t level;  // slice level: 0 = the trigger's own slice, L = out-slice of a_L
+  int8_t grp;    // delta group
+  int8_t level;  // 1..4: chain slice of a_level; kLvlDomU / kLvlDomV: trigger slice
   int8_t pad0, pad1;
   int32_t a, b;  // CSR range of the slice piece
-  int32_t path[kMaxChain];
+  int32_t path[kMaxChain];  // chain a1..a_level; domain tasks: path[0] = scratch slot
 };
 
-struct Emitter {
+struct Queue {
   Task *q;
   int32_t *count;
   int32_t cap;
-  int32_t row;
-  int32_t col;
-  bool on;
-  // cut [a, b) into kTaskSpan pieces; false (caller walks it serially) when
-  // emission is off or the queue is full.  Path by value: no address taken.
-  __device__ bool emit(int level, int p0, int p1, int p2, int p3, int p4, int a, int b) const {
-    if (!on) return false;
-    const int n = (b - a + kTaskSpan - 1) / kTaskSpan;
-    const int base = atomicAdd(count, n);
-    if (base + n > cap) {
-      for (int k = base; k < cap; ++k) q[k].row = -1;  // holes stay empty
-      return false;
-    }
-    for (int k = 0; k < n; ++k) {
-      Task t;
-      t.row = row;
-      t.col = (int8_t)col;
-      t.level = (int8_t)level;
-      t.pad0 = t.pad1 = 0;
-      t.a = a + k * kTaskSpan;
-      t.b = min(b, t.a + kTaskSpan);
-      t.path[0] = p0; t.path[1] = p1; t.path[2] = p2; t.path[3] = p3; t.path[4] = p4;
-      q[base + k] = t;
-    }
-    return true;
-  }
 };
 
-// ---------------------------------------------------------- families
-
-// FAN / DEGREE (kernels.py:290-303)
-__device__ __forceinline__ long long col_fan_degree(const Ctx &c, const DevPlan &p) {
-  const int x = p.endpoint ? c.v : c.u;
-  const Win w = p.endpoint ? (p.direction ? c.wvo : c.wvi) : (p.direction ? c.wuo : c.wui);
-  long long n = w.len() - loops_in_window(c, x);
-  if (p.exclude_trigger && c.u != c.v) n -= 1;
-  if (p.min_size > 1 && n < p.min_size) n = 0;
-  return n;
-}
-
-// cycle_2 = [u != v and v -> u in window] (kernels.py:320-322)
-__device__ __forceinline__ long long col_cycle2(const Ctx &c, const DevPlan &p) {
-  if (c.u == c.v) return 0;
-  long long raw = exists_in(c, 1, c.v, c.wvo, c.u) ? 1 : 0;
-  return raw >= p.min_size ? raw : 0;
-}
-
-// distinct windowed neighbours of x in dir over CSR range [ja, jb) with
-// stride, excluding x (self-loops) and ex
-__device__ __forceinline__ long long distinct_range(const Ctx &c, int dir, int x, int ex, int ja,
-                                                    int jb, int stride) {
-  long long n = 0;
-#pragma unroll 4
-  for (int j = ja; j < jb; j += stride) {
-    const int y = __ldg(c.g.nbr[dir] + j);
-    if (y == x || y == ex) continue;
-    n += first_in_window(c, dir, j);
+// cut [a, b) into kTaskSpan pieces; false (caller walks it itself) when the
+// queue is full — the walk is slower but exact and still on the GPU
+__device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p1, int p2, int p3,
+                     int p4, int a, int b) {
+  const int n = (b - a + kTaskSpan - 1) / kTaskSpan;
+  const int base = atomicAdd(qu.count, n);
+  if (base + n > qu.cap) {
+    for (int k = base; k < qu.cap; ++k) qu.q[k].row = -1;  // holes stay empty
+    return false;
   }
-  return n;
+  for (int k = 0; k < n; ++k) {
+    Task t;
+    t.row = row;
+    t.grp = (int8_t)grp;
+    t.level = (int8_t)level;
+    t.pad0 = t.pad1 = 0;
+    t.a = a + k * kTaskSpan;
+    t.b = min(b, t.a + kTaskSpan);
+    t.path[0] = p0; t.path[1] = p1; t.path[2] = p2; t.path[3] = p3; t.path[4] = p4;
+    qu.q[base + k] = t;
+  }
+  return true;
 }
 
-// |N^{dx}(x) ∩ N^{dy}(y)|, early exit at K (sg: x = s out, y = v in;
-// gs: x = d in, y = u out).  x and y are never members (no self-loops).
+// ------------------------------------------------------------ set helpers
+
+// distinct-neighbour intersection |N^{dx}(x) ∩ N^{dy}(y)|, early exit at K,
+// walking the shorter windowed slice (sg: x = s out, y = v in; gs: x = d
+// in, y = u out).  x and y are never members (no self-loops).
 __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, int dy,
-                                          const Win &wy, int K, Budget *bud) {
+                                          const Win &wy, int K) {
   const Win wx = window(c, dx, x);
   const bool walk_x = wx.len() <= wy.len();
   const Win w = walk_x ? wx : wy;
-  if (bud && !bud->take(2 * w.len())) return 0;
-  const int owner = walk_x ? x : y, other = walk_x ? y : x;
+  const int other = walk_x ? y : x;
   const int d = walk_x ? dx : dy, od = walk_x ? dy : dx;
   const Win ow = walk_x ? wy : wx;
   int hits = 0;
   for (int j = w.a; j < w.b && hits < K; ++j) {
     const int m = __ldg(c.g.nbr[d] + j);
-    if (m == owner || m == other || !first_in_window(c, d, j)) continue;
+    if (m == x || m == y || !first_in_window(c, d, j)) continue;
     hits += exists_in(c, od, other, ow, m);
   }
   return hits;
 }
 
-// sg entry: s = CSR in-entry j of u; #{s : |N+(s) ∩ N-(v)| >= K} (kernels.py:358-375)
-__device__ __forceinline__ int sg_entry(const Ctx &c, int K, int seg_u, int j, Budget *bud) {
-  const int s = __ldg(c.g.nbr[0] + j);
-  if (s == c.u || s == c.v || !first_in_window(c, 0, j)) return 0;
-  return inner_hits(c, s, 1, c.v, 0, c.wvi, K, bud) >= K;
-}
-
-// gs entry: d = CSR out-entry j of v; #{d : |N-(d) ∩ N+(u)| >= K} (Appendix B)
-__device__ __forceinline__ int gs_entry(const Ctx &c, int K, int seg_v, int j, Budget *bud) {
-  const int d = __ldg(c.g.nbr[1] + j);
-  if (d == c.v || d == c.u || !first_in_window(c, 1, j)) return 0;
-  return inner_hits(c, d, 0, c.u, 1, c.wuo, K, bud) >= K;
-}
-
-// closing set size for a chain ending at `a` with NP earlier chain nodes:
+// closing set of a chain ending at `a` with NP earlier chain nodes:
 //   |(N+(a) ∩ N-(u)) \ {v, path[0..NP-1]}|   (Appendix A cycle_k; cycle_4
-//   kernels.py:330-341 for NP = 0).
+//   kernels.py:330-341 for NP = 0)
 template <int NP>
-__device__ __forceinline__ int close_count(const Ctx &c, int a, const int (&path)[kMaxChain],
-                                           Budget *bud) {
+__device__ __forceinline__ int close_count(const Ctx &c, int a, const int (&path)[kMaxChain]) {
   const Win wa = window(c, 1, a);
   const bool walk_a = wa.len() <= c.wui.len();
   const Win w = walk_a ? wa : c.wui;
-  if (bud && !bud->take(2 * w.len())) return 0;
   const int d = walk_a ? 1 : 0;
   int cnt = 0;
   for (int j = w.a; j < w.b; ++j) {
@@ -307,300 +225,301 @@ __device__ __forceinline__ int close_count(const Ctx &c, int a, const int (&path
   return cnt;
 }
 
-// Fused cycle group: every CYCLE column (length 3..8) of one delta shares
-// one depth-first chain enumeration.  Depth d = chain length (number of
-// intermediate accounts a1..a_d); cycle_{d+3} is closed at depth d:
-//   a1 in N+(v)\{u};  a_i in N+(a_{i-1}) \ {u, v, a1..a_{i-2}};
-//   each chain adds |C| = close_count(a_d) when |C| >= K_{d+3}
-//   (depth 0: a = v, C = N+(v) ∩ N-(u) \ {u, v} = cycle_3, kernels.py:323-327;
-//   depth 1: cycle_4, kernels.py:328-343; depths 2..5: cycle_5..8, Appendix A).
-// Level L enumerates the entries j in [ja, jb) (stride) of the out-slice of
-// its owner (v for L = 0, else a_L = path[L-1]); the chosen node is a_{L+1}
-// at depth L+1.  A node whose window exceeds kDeepSplit is handed to the
-// emitter as tasks instead of being walked (when emission is on).
+// per-depth close: add |C| to every cycle column closing at depth d whose
+// min_size it reaches (per-binding threshold, engine.py:462-464)
 struct CycAcc {
-  long long d[kMaxChain + 1];
+  long long e[kMaxCyc];
 };
 
+__device__ __forceinline__ void close_at(const CycGroup &cg, int d, int cc, CycAcc &acc) {
+#pragma unroll
+  for (int e = 0; e < kMaxCyc; ++e)
+    if (e < cg.n && cg.depth[e] == d && cc >= cg.k[e]) acc.e[e] += cc;
+}
+
+// Chains a1..a_d of the cycle group (d <= MAXD):
+//   a1 in N+(v)\{u};  a_i in N+(a_{i-1}) \ {u, v, a1..a_{i-2}};
+//   cycle_{d+3} closes at depth d.
+// Level L walks entries j in [ja, jb) of the out-slice of a_L = path[L-1]
+// (L >= 1; level 0 is the V item loop) choosing a_{L+1}.  A chosen node
+// whose window exceeds kDeepSplit is emitted as a chain task when possible.
 template <int MAXD, int L>
-__device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg,
-                                            int (&path)[kMaxChain], int ja, int jb, int stride,
-                                            CycAcc &acc, Budget *bud, const Emitter &em) {
-  const int owner = L == 0 ? c.v : path[L > 0 ? L - 1 : 0];
-  for (int j = ja; j < jb; j += stride) {
+__device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                            int (&path)[kMaxChain], int ja, int jb, CycAcc &acc,
+                                            const Queue &qu) {
+  const int owner = path[L - 1];
+  for (int j = ja; j < jb; ++j) {
     const int a = __ldg(c.g.nbr[1] + j);
     if (a == owner || a == c.u || a == c.v) continue;
     bool dup = false;
 #pragma unroll
     for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
     if (dup || !first_in_window(c, 1, j)) continue;
-    if (cg.mask & (1 << (L + 1))) {
-      const int cc = close_count<L>(c, a, path, bud);
-      if (bud && bud->blown) return;
-      if (cc >= cg.k[L + 1]) acc.d[L + 1] += cc;
-    }
+    if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, path), acc);
     if constexpr (L + 1 < MAXD) {
       path[L] = a;
       const Win w = window(c, 1, a);
       if (w.len() > kDeepSplit &&
-          em.emit(L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b))
+          emit(qu, row, grp, L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b))
         continue;
-      if (bud && !bud->take(w.len())) return;
-      chain_level<MAXD, L + 1>(c, cg, path, w.a, w.b, 1, acc, bud, em);
-      if (bud && bud->blown) return;
+      chain_level<MAXD, L + 1>(c, cg, row, grp, path, w.a, w.b, acc, qu);
     }
   }
 }
 
-// runtime (max depth, start level) -> template instance
-__device__ __forceinline__ void cycle_chain(const Ctx &c, const CycGroup &cg, int L0,
-                                            const int (&path0)[kMaxChain], int ja, int jb,
-                                            int stride, CycAcc &acc, Budget *bud,
-                                            const Emitter &em) {
-  int path[kMaxChain] = {path0[0], path0[1], path0[2], path0[3], path0[4]};
-  switch (cg.maxd * 8 + L0) {
-#define TM_CHAIN_CASE(C_, L_) \
-  case C_ * 8 + L_: chain_level<C_, L_>(c, cg, path, ja, jb, stride, acc, bud, em); return;
-    TM_CHAIN_CASE(1, 0)
-    TM_CHAIN_CASE(2, 0) TM_CHAIN_CASE(2, 1)
-    TM_CHAIN_CASE(3, 0) TM_CHAIN_CASE(3, 1) TM_CHAIN_CASE(3, 2)
-    TM_CHAIN_CASE(4, 0) TM_CHAIN_CASE(4, 1) TM_CHAIN_CASE(4, 2) TM_CHAIN_CASE(4, 3)
-    TM_CHAIN_CASE(5, 0) TM_CHAIN_CASE(5, 1) TM_CHAIN_CASE(5, 2) TM_CHAIN_CASE(5, 3)
-    TM_CHAIN_CASE(5, 4)
+// cycles through chain node a1 = m (a V item), depths 1..maxd
+__device__ __forceinline__ void cycles_from_a1(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                               int m, CycAcc &acc, const Queue &qu) {
+  int path[kMaxChain] = {m, -1, -1, -1, -1};
+  if (cg.mask & 2) close_at(cg, 1, close_count<0>(c, m, path), acc);
+  if (cg.maxd < 2) return;
+  const Win w = window(c, 1, m);
+  if (w.len() > kDeepSplit && emit(qu, row, grp, 1, m, -1, -1, -1, -1, w.a, w.b)) return;
+  switch (cg.maxd) {
+    case 2: chain_level<2, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
+    case 3: chain_level<3, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
+    case 4: chain_level<4, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
+    default: chain_level<5, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
+  }
+}
+
+// a chain task resumes at level L with a1..a_L given
+__device__ __forceinline__ void cycles_resume(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                              int L, const int (&p0)[kMaxChain], int ja, int jb,
+                                              CycAcc &acc, const Queue &qu) {
+  int path[kMaxChain] = {p0[0], p0[1], p0[2], p0[3], p0[4]};
+  switch (cg.maxd * 8 + L) {
+#define TM_CHAIN_CASE(D_, L_) \
+  case D_ * 8 + L_: chain_level<D_, L_>(c, cg, row, grp, path, ja, jb, acc, qu); return;
+    TM_CHAIN_CASE(2, 1)
+    TM_CHAIN_CASE(3, 1) TM_CHAIN_CASE(3, 2)
+    TM_CHAIN_CASE(4, 1) TM_CHAIN_CASE(4, 2) TM_CHAIN_CASE(4, 3)
+    TM_CHAIN_CASE(5, 1) TM_CHAIN_CASE(5, 2) TM_CHAIN_CASE(5, 3) TM_CHAIN_CASE(5, 4)
 #undef TM_CHAIN_CASE
     default: return;
   }
 }
 
-// depth-0 close (cycle_3) of a group, uniform across lanes
-__device__ __forceinline__ long long cycle3_of(const Ctx &c, const CycGroup &cg, Budget *bud) {
-  if (!(cg.mask & 1)) return 0;
-  const int path[kMaxChain] = {-1, -1, -1, -1, -1};
-  const int cc = close_count<0>(c, c.v, path, bud);
-  return cc >= cg.k[0] ? cc : 0;
+// ------------------------------------------------------------ items
+//
+// A Sink receives the contributions of one item of row `owner`:
+//   col(ci, v)  additive column value      sa() / sc()  stack a / c     c3()  cycle_3 raw
+
+template <class Sink>
+__device__ __forceinline__ void u_item(const Ctx &c, const DevPlans &P, const DevGroup &gr, int j,
+                                       Sink &sk) {
+  const int m = __ldg(c.g.nbr[0] + j);
+  if (m == c.u || m == c.v || !first_in_window(c, 0, j)) return;
+  if (gr.has_stack) sk.sa();
+  if ((gr.cyc.mask & 1) && c.u != c.v && exists_in(c, 1, c.v, c.wvo, m)) sk.c3();
+  for (int i = 0; i < gr.n_sg; ++i) {  // sg: source m (kernels.py:365-374)
+    const int ci = gr.sg_col[i], K = P.p[ci].min_size;
+    if (inner_hits(c, m, 1, c.v, 0, c.wvi, K) >= K) sk.col(ci, 1);
+  }
 }
 
-// ------------------------------------------------------------- tier 1
-
-// cycle group in one thread (budgeted): acc.d[d] = column of length d + 3
-__device__ __forceinline__ void eval_cycle_group_light(const Ctx &c, const CycGroup &cg, CycAcc &acc,
-                                                       Budget &bud, const Emitter &off) {
+template <class Sink>
+__device__ __forceinline__ void v_item(const Ctx &c, const DevPlans &P, const DevGroup &gr, int grp,
+                                       int row, int j, Sink &sk, const Queue &qu) {
+  const int m = __ldg(c.g.nbr[1] + j);
+  if (m == c.u || m == c.v || !first_in_window(c, 1, j)) return;
+  if (gr.has_stack) sk.sc();
+  for (int i = 0; i < gr.n_gs; ++i) {  // gs: destination m (Appendix B)
+    const int ci = gr.gs_col[i], K = P.p[ci].min_size;
+    if (inner_hits(c, m, 0, c.u, 1, c.wuo, K) >= K) sk.col(ci, 1);
+  }
+  if (gr.cyc.maxd >= 1 && c.u != c.v && c.wui.len() > 0) {
+    CycAcc acc;
 #pragma unroll
-  for (int d = 0; d <= kMaxChain; ++d) acc.d[d] = 0;
-  if (c.u == c.v || c.wui.len() == 0 || c.wvo.len() == 0) return;
-  acc.d[0] = cycle3_of(c, cg, &bud);
-  if (bud.blown || cg.maxd == 0) return;
-  if (!bud.take(c.wvo.len())) return;
-  const int path[kMaxChain] = {-1, -1, -1, -1, -1};
-  cycle_chain(c, cg, 0, path, c.wvo.a, c.wvo.b, 1, acc, &bud, off);
-}
-
-// full column, one thread, budgeted
-__device__ __forceinline__ long long eval_light(const Ctx &c, const DevPlan &p, Budget &bud,
-                                                const Emitter &off) {
-  switch (p.family) {
-    case TM_FAN:
-    case TM_DEGREE: return col_fan_degree(c, p);
-    case TM_CYCLE:  // cycle_2 only; lengths >= 3 go through eval_cycle_group
-      return col_cycle2(c, p);
-    case TM_SG: {
-      const Win w = c.wui;
-      if (!bud.take(w.len())) return 0;
-      const int seg = __ldg(c.g.ptr[0] + c.u);
-      long long n = 0;
-      for (int j = w.a; j < w.b; ++j) {
-        n += sg_entry(c, p.min_size, seg, j, &bud);
-        if (bud.blown) return 0;
-      }
-      return n;
-    }
-    case TM_GS: {
-      const Win w = c.wvo;
-      if (!bud.take(w.len())) return 0;
-      const int seg = __ldg(c.g.ptr[1] + c.v);
-      long long n = 0;
-      for (int j = w.a; j < w.b; ++j) {
-        n += gs_entry(c, p.min_size, seg, j, &bud);
-        if (bud.blown) return 0;
-      }
-      return n;
-    }
-    case TM_STACK: {  // kernels.py:379-402
-      if (!bud.take(c.wui.len())) return 0;
-      const long long a = distinct_range(c, 0, c.u, c.v, c.wui.a, c.wui.b, 1);
-      if (a == 0 || a < p.min_size) return 0;
-      if (!bud.take(c.wvo.len())) return 0;
-      const long long d = distinct_range(c, 1, c.v, c.u, c.wvo.a, c.wvo.b, 1);
-      if (d == 0 || d < p.min_size) return 0;
-      return a * d;
-    }
-    default: return 0;
-  }
-}
-
-__global__ void __launch_bounds__(kLightThreads) k_mine_light(
-    const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans plans, int64_t lo,
-    int64_t n_rows, long long *__restrict__ out, int32_t *__restrict__ heavy_q,
-    int32_t *__restrict__ heavy_n, int budget) {
-  extern __shared__ long long stage[];  // per warp [32][plans.n] when plans.n <= kStageCols
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wrow0 = (int64_t)blockIdx.x * blockDim.x + warp * 32;
-  const int64_t row = wrow0 + lane;
-  const int C = plans.n;
-  const bool staged = C <= kStageCols;
-  long long *wstage = stage + (size_t)warp * 32 * C;
-  bool heavy = false;
-  if (row < n_rows) {
-    const int e = (int)(lo + row);
-    const int u = __ldg(g.e_src + e), v = __ldg(g.e_dst + e);
-    const uint32_t r = __ldg(g.e_rank + e);
-    Budget bud{budget, false};
-    const Emitter off{nullptr, nullptr, 0, 0, 0, false};
-    Ctx c{g, u, v, 0u, r, {}, {}, {}, {}};
-    const uint32_t *cur = nullptr;
-    long long *o = staged ? wstage + lane * C : out + row * C;
-    for (int ci = 0; ci < C; ++ci) {
-      const DevPlan &p = plans.p[ci];
-      if (p.lo_tab != cur) {  // new delta group: its windows, once
-        cur = p.lo_tab;
-        c.lo = __ldg(cur + r);
-        fill_windows(c, p.need_group);
-      }
-      if (p.family == TM_CYCLE && p.cycle_len >= 3) {
-        if (p.cyc.lead) {  // one fused enumeration writes every member column
-          CycAcc acc;
-          eval_cycle_group_light(c, p.cyc, acc, bud, off);
-          if (bud.blown) { heavy = true; break; }
+    for (int e = 0; e < kMaxCyc; ++e) acc.e[e] = 0;
+    cycles_from_a1(c, gr.cyc, row, grp, m, acc, qu);
 #pragma unroll
-          for (int d = 0; d <= kMaxChain; ++d)
-            if (p.cyc.mask & (1 << d)) o[p.cyc.col[d]] = acc.d[d];
-        }
-        continue;
-      }
-      const long long val = eval_light(c, p, bud, off);
-      if (bud.blown) { heavy = true; break; }
-      o[ci] = val;
-    }
-  }
-  if (staged) {  // coalesced write-back of the warp's 32 rows (no block barrier)
-    __syncwarp();
-    const int64_t left = n_rows - wrow0;
-    const int nrow = left < 32 ? (int)(left > 0 ? left : 0) : 32;
-    long long *dst = out + wrow0 * C;
-    for (int i = lane; i < nrow * C; i += 32) dst[i] = wstage[i];
-  }
-  // warp-aggregated append of heavy triggers (their rows are rewritten by
-  // k_mine_heavy)
-  const unsigned m = __ballot_sync(0xffffffffu, heavy);
-  if (m) {
-    int base = 0;
-    if (lane == __ffs(m) - 1) base = atomicAdd(heavy_n, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-    if (heavy) heavy_q[base + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
+    for (int e = 0; e < kMaxCyc; ++e)
+      if (e < gr.cyc.n && acc.e[e]) sk.col(gr.cyc.col[e], acc.e[e]);
   }
 }
 
-// ------------------------------------------------------------- tier 2
+// ------------------------------------------------------------ k_mine_warp
 
-// warp-uniform emission of a level-0 slice: lane 0 emits, all lanes agree
-__device__ __forceinline__ bool warp_emit(const Emitter &em, const Win &w) {
-  int ok = 0;
-  if ((threadIdx.x & 31) == 0) ok = em.emit(0, -1, -1, -1, -1, -1, w.a, w.b) ? 1 : 0;
-  return __shfl_sync(0xffffffffu, ok, 0) != 0;
-}
-
-// one warp, one heavy trigger, one column: returns the warp's partial (all
-// lanes hold it); pieces beyond kOuterSplit / kDeepSplit are emitted
-__device__ long long eval_heavy(const Ctx &c, const DevPlan &p, const Emitter &em) {
-  const int lane = threadIdx.x & 31;
-  switch (p.family) {
-    case TM_FAN:
-    case TM_DEGREE: return col_fan_degree(c, p);
-    case TM_CYCLE:  // cycle_2 only; lengths >= 3 go through the group path
-      return col_cycle2(c, p);
-    case TM_SG: {
-      if (c.wui.len() > kOuterSplit && warp_emit(em, c.wui)) return 0;
-      const int seg = __ldg(c.g.ptr[0] + c.u);
-      long long n = 0;
-      for (int j = c.wui.a + lane; j < c.wui.b; j += 32) n += sg_entry(c, p.min_size, seg, j, nullptr);
-      return warp_sum(n);
-    }
-    case TM_GS: {
-      if (c.wvo.len() > kOuterSplit && warp_emit(em, c.wvo)) return 0;
-      const int seg = __ldg(c.g.ptr[1] + c.v);
-      long long n = 0;
-      for (int j = c.wvo.a + lane; j < c.wvo.b; j += 32) n += gs_entry(c, p.min_size, seg, j, nullptr);
-      return warp_sum(n);
-    }
-    case TM_STACK: {
-      const long long a = warp_sum(distinct_range(c, 0, c.u, c.v, c.wui.a + lane, c.wui.b, 32));
-      if (a == 0 || a < p.min_size) return 0;
-      const long long d = warp_sum(distinct_range(c, 1, c.v, c.u, c.wvo.a + lane, c.wvo.b, 32));
-      if (d == 0 || d < p.min_size) return 0;
-      return a * d;
-    }
-    default: return 0;
-  }
-}
-
-struct Queues {
-  Task *q;
-  int32_t *count;
-  int32_t cap;
+struct WarpShared {
+  int u[32], v[32];
+  uint32_t lo[32], hi[32];
+  Win wui[32], wuo[32], wvi[32], wvo[32];
+  int excl[32];
+  int sa[32], sc[32], c3[32];
 };
 
-__global__ void __launch_bounds__(kHeavyThreads) k_mine_heavy(
-    const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans plans, int64_t lo,
-    long long *__restrict__ out, const int32_t *__restrict__ heavy_q,
-    const int32_t *__restrict__ heavy_n, Queues tq) {
-  const int n = *heavy_n;
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  const int lane = threadIdx.x & 31;
-  for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
-    const int row = heavy_q[i];
-    const int e = (int)(lo + row);
-    const int u = __ldg(g.e_src + e), v = __ldg(g.e_dst + e);
-    const uint32_t r = __ldg(g.e_rank + e);
-    long long *o = out + (int64_t)row * plans.n;
-    for (int ci = 0; ci < plans.n; ++ci) {
-      const DevPlan &p = plans.p[ci];
-      Ctx c{g, u, v, __ldg(p.lo_tab + r), r, {}, {}, {}, {}};
-      fill_windows(c, p.need);
-      const Emitter em{tq.q, tq.count, tq.cap, row, ci, true};
-      if (p.family == TM_CYCLE && p.cycle_len >= 3) {
-        if (!p.cyc.lead) continue;
-        // cycle group: depth 0 (cycle_3) uniform; chains spread over lanes,
-        // wide nodes / a wide first slice become tasks
-        CycAcc acc;
-#pragma unroll
-        for (int d = 0; d <= kMaxChain; ++d) acc.d[d] = 0;
-        if (c.u != c.v && c.wui.len() > 0 && c.wvo.len() > 0) {
-          acc.d[0] = cycle3_of(c, p.cyc, nullptr);
-          if (p.cyc.maxd > 0 && !(c.wvo.len() > kOuterSplit && warp_emit(em, c.wvo))) {
-            const int path[kMaxChain] = {-1, -1, -1, -1, -1};
-            cycle_chain(c, p.cyc, 0, path, c.wvo.a + lane, c.wvo.b, 32, acc, nullptr, em);
-          }
-        }
-#pragma unroll
-        for (int d = 1; d <= kMaxChain; ++d) acc.d[d] = warp_sum(acc.d[d]);
-        if (lane == 0) {
-#pragma unroll
-          for (int d = 0; d <= kMaxChain; ++d)
-            if (p.cyc.mask & (1 << d)) o[p.cyc.col[d]] = acc.d[d];
-        }
-        continue;
-      }
-      const long long val = eval_heavy(c, p, em);
-      if (lane == 0) o[ci] = val;
-    }
+struct SmemSink {  // contributions of row `owner` into the warp's shared state
+  WarpShared &ws;
+  long long *stage;
+  int owner, C;
+  __device__ __forceinline__ void col(int ci, long long v) {
+    atomicAdd(reinterpret_cast<unsigned long long *>(stage + owner * C + ci), (unsigned long long)v);
   }
+  __device__ __forceinline__ void sa() { atomicAdd(&ws.sa[owner], 1); }
+  __device__ __forceinline__ void sc() { atomicAdd(&ws.sc[owner], 1); }
+  __device__ __forceinline__ void c3() { atomicAdd(&ws.c3[owner], 1); }
+};
+
+__device__ __forceinline__ Ctx ctx_of(const DevGraph &g, const WarpShared &ws, int o) {
+  return Ctx{g, ws.u[o], ws.v[o], ws.lo[o], ws.hi[o], ws.wui[o], ws.wuo[o], ws.wvi[o], ws.wvo[o]};
 }
 
-// ------------------------------------------------------------- tier 3
+// owner lane of flattened item k: the last lane whose exclusive prefix <= k
+__device__ __forceinline__ int owner_of(const WarpShared &ws, int k) {
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1)
+    if (ws.excl[o + step] <= k) o += step;
+  return o;
+}
 
-__global__ void __launch_bounds__(kHeavyThreads) k_mine_tasks(
-    const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans plans, int64_t lo,
-    long long *__restrict__ out, Queues in, Queues next) {
+// items of slice length `len` per lane, flattened over the warp: every item
+// is processed once by `f(owner lane, index within the owner's slice)`
+template <class F>
+__device__ __forceinline__ void flat_for(WarpShared &ws, int lane, int len, F &&f) {
+  int incl = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  ws.excl[lane] = incl - len;
+  __syncwarp();
+  for (int base = 0; base < total; base += 32) {
+    const int k = base + lane;
+    if (k < total) {
+      const int o = owner_of(ws, k);
+      f(o, k - ws.excl[o]);
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kThreads) k_mine_warp(
+    const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
+    int64_t n_rows, long long *__restrict__ out, Queue qu, int32_t *__restrict__ split_rows,
+    int32_t *__restrict__ split_n, int32_t *__restrict__ scratch, int32_t split_cap) {
+  extern __shared__ long long stage_all[];  // [warp][32][C]
+  __shared__ WarpShared wsh[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpShared &ws = wsh[warp];
+  const int C = P.n;
+  long long *stage = stage_all + (size_t)warp * 32 * C;
+  const int64_t wrow0 = (int64_t)blockIdx.x * kThreads + warp * 32;
+  const int64_t row = wrow0 + lane;
+  const bool valid = row < n_rows;
+  int u = 0, v = 0;
+  uint32_t r = 0;
+  if (valid) {
+    const int e = (int)(lo + row);
+    u = __ldg(g.e_src + e);
+    v = __ldg(g.e_dst + e);
+    r = __ldg(g.e_rank + e);
+  }
+  for (int i = 0; i < C; ++i) stage[lane * C + i] = 0;
+
+  for (int gi = 0; gi < P.ngroups; ++gi) {
+    const DevGroup &gr = P.gr[gi];
+    Ctx c{g, u, v, valid ? __ldg(gr.lo_tab + r) : 1u, r, {}, {}, {}, {}};
+    if (valid) fill_windows(c, gr.need);
+    // per-lane columns: fan / degree (kernels.py:290-303), cycle_2 (:320-322)
+    if (valid) {
+      for (int i = 0; i < gr.ncols; ++i) {
+        const int ci = gr.cols[i];
+        const DevPlan &p = P.p[ci];
+        if (p.family == TM_FAN || p.family == TM_DEGREE) {
+          const int x = p.endpoint ? v : u;
+          const Win w = p.endpoint ? (p.direction ? c.wvo : c.wvi) : (p.direction ? c.wuo : c.wui);
+          long long n = w.len() - loops_in_window(c, x);
+          if (p.exclude_trigger && u != v) n -= 1;
+          if (p.min_size > 1 && n < p.min_size) n = 0;
+          stage[lane * C + ci] = n;
+        } else if (p.family == TM_CYCLE && p.cycle_len == 2) {
+          const long long raw = (u != v && exists_in(c, 1, v, c.wvo, u)) ? 1 : 0;
+          stage[lane * C + ci] = raw >= p.min_size ? raw : 0;
+        }
+      }
+    }
+    if (!gr.udom && !gr.vdom) continue;
+    ws.u[lane] = u; ws.v[lane] = v; ws.lo[lane] = c.lo; ws.hi[lane] = c.hi;
+    ws.wui[lane] = c.wui; ws.wuo[lane] = c.wuo; ws.wvi[lane] = c.wvi; ws.wvo[lane] = c.wvo;
+    ws.sa[lane] = ws.sc[lane] = ws.c3[lane] = 0;
+    // slices too long for the warp become domain tasks
+    int ulen = (valid && gr.udom) ? c.wui.len() : 0;
+    int vlen = (valid && gr.vdom) ? c.wvo.len() : 0;
+    int slot = -1;
+    if (ulen > kDomSplit || vlen > kDomSplit) {
+      if (gr.has_stack || (gr.cyc.mask & 1)) {
+        slot = atomicAdd(split_n, 1);
+        if (slot >= split_cap) {
+          slot = -2;  // no scratch left: the warp walks the slices itself
+        } else {
+          split_rows[2 * slot] = (int)row;
+          split_rows[2 * slot + 1] = gi;
+        }
+      }
+      if (slot != -2) {
+        if (ulen > kDomSplit && emit(qu, (int)row, gi, kLvlDomU, slot, -1, -1, -1, -1, c.wui.a, c.wui.b))
+          ulen = 0;
+        if (vlen > kDomSplit && emit(qu, (int)row, gi, kLvlDomV, slot, -1, -1, -1, -1, c.wvo.a, c.wvo.b))
+          vlen = 0;
+      }
+    }
+    __syncwarp();
+    flat_for(ws, lane, ulen, [&](int o, int k) {
+      const Ctx co = ctx_of(g, ws, o);
+      SmemSink sk{ws, stage, o, C};
+      u_item(co, P, gr, co.wui.a + k, sk);
+    });
+    flat_for(ws, lane, vlen, [&](int o, int k) {
+      const Ctx co = ctx_of(g, ws, o);
+      SmemSink sk{ws, stage, o, C};
+      v_item(co, P, gr, gi, (int)(wrow0 + o), co.wvo.a + k, sk, qu);
+    });
+    // whole-count columns: stack a * c (kernels.py:379-402), cycle_3 threshold
+    if (valid) {
+      const long long a = ws.sa[lane], d = ws.sc[lane], c3 = ws.c3[lane];
+      if (slot >= 0) {
+        scratch[3 * slot] = (int)a;
+        scratch[3 * slot + 1] = (int)d;
+        scratch[3 * slot + 2] = (int)c3;
+      }
+      for (int i = 0; i < gr.ncols; ++i) {
+        const int ci = gr.cols[i];
+        const DevPlan &p = P.p[ci];
+        if (p.family == TM_STACK)
+          stage[lane * C + ci] = (a > 0 && d > 0 && a >= p.min_size && d >= p.min_size) ? a * d : 0;
+        else if (p.family == TM_CYCLE && p.cycle_len == 3)
+          stage[lane * C + ci] = c3 >= p.min_size ? c3 : 0;
+      }
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  const int64_t left = n_rows - wrow0;
+  const int nrow = left < 32 ? (int)(left > 0 ? left : 0) : 32;
+  long long *dst = out + wrow0 * C;
+  for (int i = lane; i < nrow * C; i += 32) dst[i] = stage[i];
+}
+
+// ------------------------------------------------------------ tasks
+
+struct GlobalSink {  // contributions of one task item, straight to global memory
+  long long *orow;
+  int32_t *scr;  // scratch slot of the row (stack a, c, cycle_3 raw)
+  __device__ __forceinline__ void col(int ci, long long v) {
+    atomicAdd(reinterpret_cast<unsigned long long *>(orow + ci), (unsigned long long)v);
+  }
+  __device__ __forceinline__ void sa() { atomicAdd(scr, 1); }
+  __device__ __forceinline__ void sc() { atomicAdd(scr + 1, 1); }
+  __device__ __forceinline__ void c3() { atomicAdd(scr + 2, 1); }
+};
+
+__global__ void __launch_bounds__(kTaskThreads) k_mine_tasks(
+    const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
+    long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next) {
   const int n = min(*in.count, in.cap);
   const int warps = gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -608,38 +527,53 @@ __global__ void __launch_bounds__(kHeavyThreads) k_mine_tasks(
     const Task t = in.q[i];
     if (t.row < 0) continue;
     const int e = (int)(lo + t.row);
-    const int u = __ldg(g.e_src + e), v = __ldg(g.e_dst + e);
+    const DevGroup &gr = P.gr[t.grp];
     const uint32_t r = __ldg(g.e_rank + e);
-    const DevPlan &p = plans.p[t.col];
-    Ctx c{g, u, v, __ldg(p.lo_tab + r), r, {}, {}, {}, {}};
-    fill_windows(c, p.need);
-    const Emitter em{next.q, next.count, next.cap, t.row, t.col, true};
-    long long part = 0;
-    if (p.family == TM_SG) {
-      const int seg = __ldg(g.ptr[0] + u);
-      for (int j = t.a + lane; j < t.b; j += 32) part += sg_entry(c, p.min_size, seg, j, nullptr);
-    } else if (p.family == TM_GS) {
-      const int seg = __ldg(g.ptr[1] + v);
-      for (int j = t.a + lane; j < t.b; j += 32) part += gs_entry(c, p.min_size, seg, j, nullptr);
-    } else if (p.family == TM_CYCLE) {  // group lead: per-depth partials
-      const int path[kMaxChain] = {t.path[0], t.path[1], t.path[2], t.path[3], t.path[4]};
+    Ctx c{g, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {}};
+    fill_windows(c, gr.need);
+    long long *orow = out + (int64_t)t.row * P.n;
+    if (t.level == kLvlDomU || t.level == kLvlDomV) {
+      GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
+      for (int j = t.a + lane; j < t.b; j += 32) {
+        if (t.level == kLvlDomU) u_item(c, P, gr, j, sk);
+        else v_item(c, P, gr, t.grp, t.row, j, sk, next);
+      }
+    } else {  // chain task: resume the enumeration at level t.level
       CycAcc acc;
 #pragma unroll
-      for (int d = 0; d <= kMaxChain; ++d) acc.d[d] = 0;
-      cycle_chain(c, p.cyc, t.level, path, t.a + lane, t.b, 32, acc, nullptr, em);
+      for (int k = 0; k < kMaxCyc; ++k) acc.e[k] = 0;
+      const int path[kMaxChain] = {t.path[0], t.path[1], t.path[2], t.path[3], t.path[4]};
+      for (int j = t.a + lane; j < t.b; j += 32)  // one entry per lane per step
+        cycles_resume(c, gr.cyc, t.row, t.grp, t.level, path, j, j + 1, acc, next);
 #pragma unroll
-      for (int d = 1; d <= kMaxChain; ++d) {
-        const long long s = warp_sum(acc.d[d]);
-        if (lane == 0 && s)
-          atomicAdd(reinterpret_cast<unsigned long long *>(out + (int64_t)t.row * plans.n + p.cyc.col[d]),
-                    (unsigned long long)s);
+      for (int k = 0; k < kMaxCyc; ++k) {
+        const long long s = warp_sum(acc.e[k]);
+        if (lane == 0 && k < gr.cyc.n && s)
+          atomicAdd(reinterpret_cast<unsigned long long *>(orow + gr.cyc.col[k]), (unsigned long long)s);
       }
-      continue;
     }
-    part = warp_sum(part);
-    if (lane == 0 && part)
-      atomicAdd(reinterpret_cast<unsigned long long *>(out + (int64_t)t.row * plans.n + t.col),
-                (unsigned long long)part);
+  }
+}
+
+// rows whose slices went to domain tasks: whole-count columns from scratch
+__global__ void k_mine_finalize(const __grid_constant__ DevPlans P, long long *__restrict__ out,
+                                const int32_t *__restrict__ split_rows,
+                                const int32_t *__restrict__ split_n, const int32_t *__restrict__ scratch,
+                                int32_t split_cap) {
+  const int n = min(*split_n, split_cap);
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const int row = split_rows[2 * s], gi = split_rows[2 * s + 1];
+    const long long a = scratch[3 * s], d = scratch[3 * s + 1], c3 = scratch[3 * s + 2];
+    const DevGroup &gr = P.gr[gi];
+    long long *orow = out + (int64_t)row * P.n;
+    for (int i = 0; i < gr.ncols; ++i) {
+      const int ci = gr.cols[i];
+      const DevPlan &p = P.p[ci];
+      if (p.family == TM_STACK)
+        orow[ci] = (a > 0 && d > 0 && a >= p.min_size && d >= p.min_size) ? a * d : 0;
+      else if (p.family == TM_CYCLE && p.cycle_len == 3)
+        orow[ci] = c3 >= p.min_size ? c3 : 0;
+    }
   }
 }
 
@@ -664,40 +598,6 @@ __global__ void k_lo_table(const int64_t *__restrict__ uniq, int64_t R, long lon
 }  // namespace tmb
 
 using namespace tmb;
-
-// pipeline depth; TM_CHUNKS (1..4) overrides it for tuning sweeps
-static int pipeline_chunks(int64_t rows) {
-  static int forced = [] {
-    const char *e = getenv("TM_CHUNKS");
-    const int v = e ? atoi(e) : 0;
-    return v >= 1 && v <= kMaxChunks ? v : 0;
-  }();
-  if (forced) return forced;
-  (void)rows;
-  return 1;  // measured: overlap loses to the extra per-chunk tail rounds at HI-Small
-}
-
-// side stream + events of the chunk pipeline (created once per graph)
-static int ensure_pipeline(tm_graph *g) {
-  if (g->side) return TM_OK;
-  TM_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
-  TM_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
-  TM_CUDA(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
-  for (int i = 0; i < 3; ++i) TM_CUDA(cudaEventCreate(&g->ev[i]));
-  for (int c = 0; c < kMaxChunks; ++c)
-    for (int i = 0; i < 4; ++i) TM_CUDA(cudaEventCreate(&g->pev[c][i]));
-  return TM_OK;
-}
-
-// light-tier work budget; TM_LIGHT_BUDGET overrides it for tuning sweeps
-static int light_budget() {
-  static int b = [] {
-    const char *e = getenv("TM_LIGHT_BUDGET");
-    const int v = e ? atoi(e) : 0;
-    return v > 0 ? v : kLightBudget;
-  }();
-  return b;
-}
 
 extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
                        int64_t *out, int out_on_device, void *stream) {
@@ -729,83 +629,62 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
   const int64_t launches0 = tm_kernel_launch_count();
 
-  // distinct deltas -> window lower-bound tables
-  int64_t deltas[kMaxPlans];
-  int slot_of[kMaxPlans];
-  int nd = 0;
+  // delta groups (one window set + one lower-bound table per distinct delta)
+  DevPlans dp{};
+  dp.n = n_plans;
+  int64_t deltas[kMaxGroups];
   for (int i = 0; i < n_plans; ++i) {
+    // same delta -> same group, unless its cycle enumeration is full
+    const bool cyc = plans[i].family == TM_CYCLE && plans[i].cycle_len >= 3;
     int k = 0;
-    while (k < nd && deltas[k] != plans[i].delta) ++k;
-    if (k == nd) deltas[nd++] = plans[i].delta;
-    slot_of[i] = k;
+    while (k < dp.ngroups && (deltas[k] != plans[i].delta || (cyc && dp.gr[k].cyc.n == kMaxCyc))) ++k;
+    if (k == dp.ngroups) {
+      if (dp.ngroups == kMaxGroups)
+        return fail(TM_E_UNSUPPORTED_PLAN, "more than " + std::to_string(kMaxGroups) +
+                                               " column groups (distinct deltas, or > " +
+                                               std::to_string(kMaxCyc) +
+                                               " cycle columns per delta) in one tm_mine call");
+      deltas[dp.ngroups++] = plans[i].delta;
+    }
+    const tm_plan_desc &p = plans[i];
+    dp.p[i] = DevPlan{p.family, p.endpoint, p.direction, p.exclude_trigger, p.cycle_len, p.min_size, k};
+    DevGroup &gr = dp.gr[k];
+    gr.cols[gr.ncols++] = (int8_t)i;
+    switch (p.family) {
+      case TM_FAN:
+      case TM_DEGREE: gr.need |= 1 << (2 * p.endpoint + p.direction); break;
+      case TM_CYCLE:
+        gr.need |= p.cycle_len == 2 ? 8 : (1 | 8);
+        if (p.cycle_len >= 3) {
+          CycGroup &cg = gr.cyc;
+          const int d = p.cycle_len - 3;
+          cg.depth[cg.n] = (int8_t)d;
+          cg.k[cg.n] = p.min_size;
+          cg.col[cg.n] = (int8_t)i;
+          cg.n++;
+          cg.mask |= 1 << d;
+          cg.maxd = std::max(cg.maxd, d);
+          if (d == 0) gr.udom = 1; else gr.vdom = 1;
+        }
+        break;
+      case TM_SG: gr.need |= 1 | 4; gr.udom = 1; gr.sg_col[gr.n_sg++] = (int8_t)i; break;
+      case TM_GS: gr.need |= 8 | 2; gr.vdom = 1; gr.gs_col[gr.n_gs++] = (int8_t)i; break;
+      case TM_STACK: gr.need |= 1 | 8; gr.udom = gr.vdom = 1; gr.has_stack = 1; break;
+      default: break;
+    }
   }
   const int64_t R = g->n_ranks;
   int rc;
-  if ((rc = g->lo_tabs.ensure(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * nd))) return rc;
-  for (int k = 0; k < nd; ++k) {
+  if ((rc = g->lo_tabs.ensure(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups))) return rc;
+  int rounds = 0;
+  for (int k = 0; k < dp.ngroups; ++k) {
+    dp.gr[k].lo_tab = g->lo_tabs.as<uint32_t>() + (size_t)k * R;
     k_lo_table<<<grid_for(R, 256), 256, 0, s>>>(g->uniq_time.as<int64_t>(), R, deltas[k],
                                                 g->lo_tabs.as<uint32_t>() + (size_t)k * R);
     TM_LAUNCHED("k_lo_table");
-  }
-  DevPlans dp{};
-  dp.n = n_plans;
-  auto need_of = [](const tm_plan_desc &p) -> int {
-    switch (p.family) {
-      case TM_FAN:
-      case TM_DEGREE: return 1 << (2 * p.endpoint + p.direction);
-      case TM_CYCLE: return p.cycle_len == 2 ? 8 : (1 | 8);
-      case TM_SG: return 1 | 4;
-      case TM_GS: return 8 | 2;
-      case TM_STACK: return 1 | 8;
-      default: return 0;
-    }
-  };
-  int rounds = 0;
-  for (int i = 0; i < n_plans; ++i) {
-    const tm_plan_desc &p = plans[i];
-    dp.p[i] = DevPlan{p.family, p.endpoint, p.direction, p.exclude_trigger, p.cycle_len,
-                      p.min_size, need_of(p), 0, g->lo_tabs.as<uint32_t>() + (size_t)slot_of[i] * R};
-    if (!(p.family == TM_FAN || p.family == TM_DEGREE ||
-          (p.family == TM_CYCLE && p.cycle_len == 2)))
-      dp.needs_sets = 1;
-    // task rounds: level-0 pieces (sg/gs/cycle) + one per deeper chain level
-    if (p.family == TM_SG || p.family == TM_GS) rounds = std::max(rounds, 1);
-    if (p.family == TM_CYCLE && p.cycle_len >= 4) rounds = std::max(rounds, p.cycle_len - 3);
-  }
-  // fused cycle groups: CYCLE columns of length >= 3 sharing a delta
-  for (int i = 0; i < n_plans; ++i) {
-    if (!(plans[i].family == TM_CYCLE && plans[i].cycle_len >= 3)) continue;
-    CycGroup cg{};
-    int lead = -1;
-    for (int k = 0; k < n_plans; ++k) {
-      if (!(plans[k].family == TM_CYCLE && plans[k].cycle_len >= 3) || slot_of[k] != slot_of[i]) continue;
-      const int d = plans[k].cycle_len - 3;
-      if (cg.mask & (1 << d)) continue;  // duplicate length: first column owns it
-      if (lead < 0) lead = k;
-      cg.mask |= 1 << d;
-      cg.k[d] = plans[k].min_size;
-      cg.col[d] = (int8_t)k;
-      cg.maxd = std::max(cg.maxd, d);
-    }
-    cg.lead = (lead == i) ? 1 : 0;
-    const int d = plans[i].cycle_len - 3;
-    if (cg.col[d] != i) {  // duplicate of an earlier same-length column: own group
-      CycGroup solo{};
-      solo.mask = 1 << d;
-      solo.k[d] = plans[i].min_size;
-      solo.col[d] = (int8_t)i;
-      solo.maxd = d;
-      solo.lead = 1;
-      cg = solo;
-    }
-    dp.p[i].cyc = cg;
-  }
-
-  for (int i = 0; i < n_plans; ++i) {  // union of needs per delta group
-    int m = 0;
-    for (int k = 0; k < n_plans; ++k)
-      if (slot_of[k] == slot_of[i]) m |= dp.p[k].need;
-    dp.p[i].need_group = m;
+    // task rounds: domain tasks, then one per chain level below a1
+    if (dp.gr[k].udom || dp.gr[k].vdom)
+      rounds = std::max(rounds, 1 + std::max(0, dp.gr[k].cyc.maxd - 1));
   }
 
   long long *d_out;
@@ -815,69 +694,50 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     if ((rc = g->out_scratch.ensure(sizeof(long long) * (size_t)rows * n_plans))) return rc;
     d_out = g->out_scratch.as<long long>();
   }
-  // Pipeline: the trigger range is cut into `nch` chunks; chunk i's light
-  // kernel runs on stream s while chunk i-1's heavy + task kernels run on the
-  // graph's side stream, so the warp-level tail work overlaps the
-  // thread-level bulk of the next chunk.  Rows of different chunks are
-  // disjoint; every chunk has its own heavy-queue slice and counter, the task
-  // queues are reused in side-stream order.
-  const int nch = pipeline_chunks(rows);
-  const int64_t task_cap = std::min<int64_t>(std::max<int64_t>(1 << 20, rows / 2), 1 << 24);
-  if ((rc = g->heavy_n.ensure(sizeof(int32_t) * (kMaxChunks + 2))) ||
-      (rc = g->heavy_q.ensure(sizeof(int32_t) * (size_t)rows)) ||
+  const int64_t task_cap = std::min<int64_t>(std::max<int64_t>(1 << 18, rows / 8), 1 << 24);
+  const int64_t split_cap = std::min<int64_t>(std::max<int64_t>(1 << 16, rows / 16), 1 << 22);
+  if ((rc = g->heavy_n.ensure(sizeof(int32_t) * 4)) ||
+      (rc = g->heavy_q.ensure(sizeof(int32_t) * 2 * (size_t)split_cap)) ||
+      (rc = g->split_scratch.ensure(sizeof(int32_t) * 3 * (size_t)split_cap)) ||
       (rc = g->tasks.ensure(sizeof(Task) * (size_t)task_cap * 2)))
     return rc;
-  if ((rc = ensure_pipeline(g))) return rc;
-  int32_t *cnt = g->heavy_n.as<int32_t>();  // [0..kMaxChunks) heavy rows, then task queues A/B
-  TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (kMaxChunks + 2), s));
-  Queues qa{g->tasks.as<Task>(), cnt + kMaxChunks, (int32_t)task_cap};
-  Queues qb{g->tasks.as<Task>() + task_cap, cnt + kMaxChunks + 1, (int32_t)task_cap};
-  cudaStream_t s2 = g->side;
-  TM_CUDA(cudaEventRecord(g->ev_fork, s));
-  TM_CUDA(cudaStreamWaitEvent(s2, g->ev_fork, 0));
+  int32_t *cnt = g->heavy_n.as<int32_t>();  // [0] split rows, [1] [2] task queues A / B
+  TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
+  Queue qa{g->tasks.as<Task>(), cnt + 1, (int32_t)task_cap};
+  Queue qb{g->tasks.as<Task>() + task_cap, cnt + 2, (int32_t)task_cap};
 
   const DevGraph dg = g->dev();
   g->prof_pending = g->prof;
-  g->prof_chunks = nch;
   if (g->prof) TM_CUDA(cudaEventRecord(g->ev[0], s));
-  const size_t smem = n_plans <= kStageCols ? sizeof(long long) * kLightThreads * n_plans : 0;
-  const int heavy_grid = 148 * (2048 / kHeavyThreads);
-  const int64_t per = (rows + nch - 1) / nch;
-  for (int ch = 0; ch < nch; ++ch) {
-    const int64_t r0 = std::min<int64_t>(rows, ch * per), r1 = std::min<int64_t>(rows, r0 + per);
-    if (r1 <= r0) continue;
-    int32_t *hq = g->heavy_q.as<int32_t>() + r0;
-    if (g->prof) TM_CUDA(cudaEventRecord(g->pev[ch][0], s));
-    k_mine_light<<<grid_for(r1 - r0, kLightThreads), kLightThreads, smem, s>>>(
-        dg, dp, lo + r0, r1 - r0, d_out + r0 * n_plans, hq, cnt + ch, light_budget());
-    TM_LAUNCHED("k_mine_light");
-    TM_CUDA(cudaEventRecord(g->pev[ch][1], s));
-    if (!dp.needs_sets) continue;
-    TM_CUDA(cudaStreamWaitEvent(s2, g->pev[ch][1], 0));
-    if (g->prof) TM_CUDA(cudaEventRecord(g->pev[ch][2], s2));
-    TM_CUDA(cudaMemsetAsync(qa.count, 0, sizeof(int32_t), s2));
-    k_mine_heavy<<<heavy_grid, kHeavyThreads, 0, s2>>>(dg, dp, lo + r0, d_out + r0 * n_plans, hq,
-                                                       cnt + ch, qa);
-    TM_LAUNCHED("k_mine_heavy");
-    Queues a = qa, b = qb;
-    for (int r = 0; r < rounds; ++r) {
-      TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int32_t), s2));
-      k_mine_tasks<<<heavy_grid, kHeavyThreads, 0, s2>>>(dg, dp, lo + r0, d_out + r0 * n_plans, a, b);
-      TM_LAUNCHED("k_mine_tasks");
-      std::swap(a, b);
-    }
-    if (g->prof) TM_CUDA(cudaEventRecord(g->pev[ch][3], s2));
+  const size_t smem = sizeof(long long) * kThreads * n_plans;
+  if (smem > 48 * 1024)
+    TM_CUDA(cudaFuncSetAttribute(k_mine_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_mine_warp<<<grid_for(rows, kThreads), kThreads, smem, s>>>(
+      dg, dp, lo, rows, d_out, qa, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
+      (int32_t)split_cap);
+  TM_LAUNCHED("k_mine_warp");
+  if (g->prof) TM_CUDA(cudaEventRecord(g->ev[1], s));
+  const int task_grid = 148 * (2048 / kTaskThreads);
+  for (int r = 0; r < rounds; ++r) {
+    TM_CUDA(cudaMemsetAsync(qb.count, 0, sizeof(int32_t), s));
+    k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dp, lo, d_out, g->split_scratch.as<int32_t>(),
+                                                    qa, qb);
+    TM_LAUNCHED("k_mine_tasks");
+    std::swap(qa, qb);
   }
-  TM_CUDA(cudaEventRecord(g->ev_join, s2));
-  TM_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
+  if (rounds > 0) {
+    k_mine_finalize<<<148, 256, 0, s>>>(dp, d_out, g->heavy_q.as<int32_t>(), cnt,
+                                        g->split_scratch.as<int32_t>(), (int32_t)split_cap);
+    TM_LAUNCHED("k_mine_finalize");
+  }
   if (g->prof) TM_CUDA(cudaEventRecord(g->ev[2], s));
   if (!out_on_device) {
     TM_CUDA(cudaMemcpyAsync(out, d_out, sizeof(long long) * (size_t)rows * n_plans,
                             cudaMemcpyDeviceToHost, s));
-    int32_t nh[kMaxChunks] = {0, 0, 0, 0};
-    TM_CUDA(cudaMemcpyAsync(nh, cnt, sizeof(nh), cudaMemcpyDeviceToHost, s));
+    int32_t nh = 0;
+    TM_CUDA(cudaMemcpyAsync(&nh, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     TM_CUDA(cudaStreamSynchronize(s));
-    g->last.heavy_triggers = (int64_t)nh[0] + nh[1] + nh[2] + nh[3];
+    g->last.heavy_triggers = nh;
   } else {
     g->last.heavy_triggers = -1;  // not read back on the async path
   }
@@ -890,14 +750,8 @@ extern "C" int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats) {
   if (g->prof_pending) {
     TM_CUDA(cudaSetDevice(g->device));
     TM_CUDA(cudaEventSynchronize(g->ev[2]));
-    float lt = 0.f, ht = 0.f, x = 0.f;
-    for (int ch = 0; ch < g->prof_chunks; ++ch) {
-      if (cudaEventElapsedTime(&x, g->pev[ch][0], g->pev[ch][1]) == cudaSuccess) lt += x;
-      if (cudaEventElapsedTime(&x, g->pev[ch][2], g->pev[ch][3]) == cudaSuccess) ht += x;
-    }
-    cudaGetLastError();  // chunks without heavy work leave their events unrecorded
-    g->last.light_ms = lt;
-    g->last.heavy_ms = ht;
+    TM_CUDA(cudaEventElapsedTime(&g->last.light_ms, g->ev[0], g->ev[1]));
+    TM_CUDA(cudaEventElapsedTime(&g->last.heavy_ms, g->ev[1], g->ev[2]));
     TM_CUDA(cudaEventElapsedTime(&g->last.total_ms, g->ev[0], g->ev[2]));
     g->prof_pending = false;
   }
@@ -908,8 +762,8 @@ extern "C" int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats) {
 extern "C" int tm_set_profiling(tm_graph *g, int on) {
   if (!g) return fail(TM_E_BAD_ARG, "NULL graph");
   TM_CUDA(cudaSetDevice(g->device));
-  int rc;
-  if ((rc = ensure_pipeline(g))) return rc;
+  for (int i = 0; i < 3; ++i)
+    if (!g->ev[i]) TM_CUDA(cudaEventCreate(&g->ev[i]));
   g->prof = on != 0;
   return TM_OK;
 }
