@@ -120,7 +120,9 @@ __device__ __forceinline__ bool first_in_window(const Ctx &c, int dir, int j) {
 }
 
 // does x's dir-window w contain neighbour n?  Windows are time-local and
-// short: scan them; bisect the pair run when w is wide.
+// short: scan them.  A wide w (a hub) is answered by one bisection of the
+// SHORTER pair run: x's dir run keyed by n, or n's opposite run keyed by x
+// (n in N^dir(x)  <=>  x in N^{1-dir}(n)).
 constexpr int kScanWin = 16;
 __device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
   if (w.len() <= kScanWin) {
@@ -128,10 +130,14 @@ __device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Wi
     for (int j = w.a; j < w.b && !hit; ++j) hit = __ldg(c.g.nbr[dir] + j) == n;
     return hit;
   }
-  const int s = __ldg(c.g.ptr[dir] + x), e = __ldg(c.g.ptr[dir] + x + 1);
-  const uint64_t base = (uint64_t)(uint32_t)n << c.g.rank_bits;
-  const int q = lb_u64(c.g.pkey[dir], s, e, base + c.lo);
-  return q < e && __ldg(c.g.pkey[dir] + q) <= base + c.hi;
+  const int xs = __ldg(c.g.ptr[dir] + x), xe = __ldg(c.g.ptr[dir] + x + 1);
+  const int ns = __ldg(c.g.ptr[dir ^ 1] + n), ne = __ldg(c.g.ptr[dir ^ 1] + n + 1);
+  const bool from_x = xe - xs <= ne - ns;
+  const uint64_t *k = c.g.pkey[from_x ? dir : dir ^ 1];
+  const int s = from_x ? xs : ns, e = from_x ? xe : ne;
+  const uint64_t base = (uint64_t)(uint32_t)(from_x ? n : x) << c.g.rank_bits;
+  const int q = lb_u64(k, s, e, base + c.lo);
+  return q < e && __ldg(k + q) <= base + c.hi;
 }
 
 __device__ __forceinline__ long long warp_sum(long long x) {
@@ -207,8 +213,8 @@ __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, in
 //   |(N+(a) ∩ N-(u)) \ {v, path[0..NP-1]}|   (Appendix A cycle_k; cycle_4
 //   kernels.py:330-341 for NP = 0)
 template <int NP>
-__device__ __forceinline__ int close_count(const Ctx &c, int a, const int (&path)[kMaxChain]) {
-  const Win wa = window(c, 1, a);
+__device__ __forceinline__ int close_count(const Ctx &c, int a, const Win &wa,
+                                           const int (&path)[kMaxChain]) {
   const bool walk_a = wa.len() <= c.wui.len();
   const Win w = walk_a ? wa : c.wui;
   const int d = walk_a ? 1 : 0;
@@ -255,10 +261,10 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
 #pragma unroll
     for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
     if (dup || !first_in_window(c, 1, j)) continue;
-    if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, path), acc);
+    const Win w = window(c, 1, a);  // a's out-window: closes and descends
+    if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, w, path), acc);
     if constexpr (L + 1 < MAXD) {
       path[L] = a;
-      const Win w = window(c, 1, a);
       if (w.len() > kDeepSplit &&
           emit(qu, row, grp, L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b))
         continue;
@@ -271,9 +277,9 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
 __device__ __forceinline__ void cycles_from_a1(const Ctx &c, const CycGroup &cg, int row, int grp,
                                                int m, CycAcc &acc, const Queue &qu) {
   int path[kMaxChain] = {m, -1, -1, -1, -1};
-  if (cg.mask & 2) close_at(cg, 1, close_count<0>(c, m, path), acc);
-  if (cg.maxd < 2) return;
   const Win w = window(c, 1, m);
+  if (cg.mask & 2) close_at(cg, 1, close_count<0>(c, m, w, path), acc);
+  if (cg.maxd < 2) return;
   if (w.len() > kDeepSplit && emit(qu, row, grp, 1, m, -1, -1, -1, -1, w.a, w.b)) return;
   switch (cg.maxd) {
     case 2: chain_level<2, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
