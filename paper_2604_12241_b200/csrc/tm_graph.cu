@@ -151,6 +151,23 @@ __global__ void k_gather_time(const uint32_t *__restrict__ rnk, const int64_t *_
 
 }  // namespace
 
+int DevBuf::ensure_on(size_t n, cudaStream_t s) {
+  if (n <= bytes && p) return TM_OK;
+  release();
+  cudaError_t e = cudaMallocAsync(&p, n ? n : 16, s);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? TM_E_OOM : TM_E_CUDA,
+                std::string("device allocation of ") + std::to_string(n) +
+                    " bytes failed: " + cudaGetErrorString(e));
+  }
+  bytes = n ? n : 16;
+  pooled = true;
+  pool_stream = s;
+  return TM_OK;
+}
+
 int DevBuf::ensure(size_t n) {
   if (n <= bytes && p) return TM_OK;
   release();
@@ -197,7 +214,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
   const int64_t *d_src = src, *d_dst = dst, *d_time = time;
   if (!on_device && E > 0) {
     int rc;
-    if ((rc = in_src.ensure(8 * E)) || (rc = in_dst.ensure(8 * E)) || (rc = in_time.ensure(8 * E)))
+    if ((rc = in_src.ensure_on(8 * E, s)) || (rc = in_dst.ensure_on(8 * E, s)) || (rc = in_time.ensure_on(8 * E, s)))
       return rc;
     TM_CUDA(cudaMemcpyAsync(in_src.p, src, 8 * E, cudaMemcpyHostToDevice, s));
     TM_CUDA(cudaMemcpyAsync(in_dst.p, dst, 8 * E, cudaMemcpyHostToDevice, s));
@@ -209,19 +226,21 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
 
   int rc;
   const int64_t Ea = E > 0 ? E : 1;
-  if ((rc = g->e_src.ensure(4 * Ea)) || (rc = g->e_dst.ensure(4 * Ea)) ||
-      (rc = g->e_rank.ensure(4 * Ea)) || (rc = g->loop.ensure(N > 0 ? N : 1)))
+  if ((rc = g->maxdeg.ensure_on(16, s))) return rc;
+  TM_CUDA(cudaMemsetAsync(g->maxdeg.p, 0, 16, s));
+  if ((rc = g->e_src.ensure_on(4 * Ea, s)) || (rc = g->e_dst.ensure_on(4 * Ea, s)) ||
+      (rc = g->e_rank.ensure_on(4 * Ea, s)) || (rc = g->loop.ensure_on(N > 0 ? N : 1, s)))
     return rc;
   TM_CUDA(cudaMemsetAsync(g->loop.p, 0, N > 0 ? N : 1, s));
   for (int d = 0; d < 2; ++d) {
-    if ((rc = g->ptr[d].ensure(4 * (N + 1))) || (rc = g->nbr[d].ensure(4 * Ea)) ||
-        (rc = g->rnk[d].ensure(4 * Ea)) || (rc = g->eid[d].ensure(4 * Ea)) ||
-        (rc = g->pkey[d].ensure(8 * Ea)) || (rc = g->prev[d].ensure(4 * Ea)))
+    if ((rc = g->ptr[d].ensure_on(4 * (N + 1), s)) || (rc = g->nbr[d].ensure_on(4 * Ea, s)) ||
+        (rc = g->rnk[d].ensure_on(4 * Ea, s)) || (rc = g->eid[d].ensure_on(4 * Ea, s)) ||
+        (rc = g->pkey[d].ensure_on(8 * Ea, s)) || (rc = g->prev[d].ensure_on(4 * Ea, s)))
       return rc;
   }
   if (E == 0) {
     for (int d = 0; d < 2; ++d) TM_CUDA(cudaMemsetAsync(g->ptr[d].p, 0, 4 * (N + 1), s));
-    if ((rc = g->uniq_time.ensure(8))) return rc;
+    if ((rc = g->uniq_time.ensure_on(8, s))) return rc;
     g->n_ranks = 0;
     g->rank_bits = 1;
     g->node_bits = std::max(1, bits_for((uint64_t)(N > 0 ? N - 1 : 0)));
@@ -231,7 +250,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
   // 1. validate ids, time range, self-loops
   ScanStats h0{LLONG_MAX, LLONG_MIN, 0, 0}, h1{};
   DevBuf st;
-  if ((rc = st.ensure(sizeof(ScanStats)))) return rc;
+  if ((rc = st.ensure_on(sizeof(ScanStats), s))) return rc;
   TM_CUDA(cudaMemcpyAsync(st.p, &h0, sizeof(ScanStats), cudaMemcpyHostToDevice, s));
   k_validate<<<1184, kB, 0, s>>>(d_src, d_dst, d_time, E, N, st.as<ScanStats>());
   TM_LAUNCHED("k_validate");
@@ -242,14 +261,14 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
 
   // 2. narrow ids, time keys
   DevBuf ka, kb, va, vb;
-  if ((rc = ka.ensure(8 * E)) || (rc = kb.ensure(8 * E)) || (rc = va.ensure(4 * E)) ||
-      (rc = vb.ensure(4 * E)))
+  if ((rc = ka.ensure_on(8 * E, s)) || (rc = kb.ensure_on(8 * E, s)) || (rc = va.ensure_on(4 * E, s)) ||
+      (rc = vb.ensure_on(4 * E, s)))
     return rc;
   k_prepare<<<grid_for(E, kB), kB, 0, s>>>(d_src, d_dst, d_time, E, h1.tmin, g->e_src.as<int32_t>(),
                                            g->e_dst.as<int32_t>(), ka.as<uint64_t>(),
                                            va.as<uint32_t>(), g->loop.as<uint8_t>());
   TM_LAUNCHED("k_prepare");
-  in_src.release();  // stream-ordered: cudaFree syncs the device
+  in_src.release();  // stream-ordered frees (memory pool): no device sync
   in_dst.release();
   in_time.release();
 
@@ -276,7 +295,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
     last_flag = (E == 1 || k_last != k_prev) ? 1u : 0u;
   }
   g->n_ranks = (int64_t)last_excl + last_flag;
-  if ((rc = g->uniq_time.ensure(8 * g->n_ranks))) return rc;
+  if ((rc = g->uniq_time.ensure_on(8 * g->n_ranks, s))) return rc;
   k_rank_scatter<<<grid_for(E, kB), kB, 0, s>>>(ks, vs, flags, E, h1.tmin,
                                                 g->uniq_time.as<int64_t>(), g->e_rank.as<uint32_t>());
   TM_LAUNCHED("k_rank_scatter");
@@ -313,14 +332,10 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
                                                g->rnk[d].as<uint32_t>(), E, g->rank_bits,
                                                g->pkey[d].as<uint64_t>(), g->prev[d].as<uint32_t>());
     TM_LAUNCHED("k_pair_fill");
-    unsigned long long *md = reinterpret_cast<unsigned long long *>(st.p);
+    unsigned long long *md = g->maxdeg.as<unsigned long long>() + d;  // read lazily by info
     TM_CUDA(cudaMemsetAsync(md, 0, 8, s));
     k_max_degree<<<592, kB, 0, s>>>(g->ptr[d].as<int32_t>(), N, md);
     TM_LAUNCHED("k_max_degree");
-    unsigned long long mh = 0;
-    TM_CUDA(cudaMemcpyAsync(&mh, md, 8, cudaMemcpyDeviceToHost, s));
-    TM_CUDA(cudaStreamSynchronize(s));
-    g->max_deg[d] = (int64_t)mh;
   }
   TM_CUDA(cudaStreamSynchronize(s));
   return TM_OK;
@@ -339,6 +354,14 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
   TM_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(TM_E_BAD_ARG, "bad device ordinal");
   TM_CUDA(cudaSetDevice(device));
+  {  // keep freed pool memory cached: rebuilding a graph then costs no cudaMalloc
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   tm_graph *g = new tm_graph();
   g->device = device;
   g->n_nodes = n_nodes;
@@ -375,8 +398,14 @@ extern "C" int tm_graph_info_get(const tm_graph *g, tm_graph_info *info) {
   info->n_nodes = g->n_nodes;
   info->n_edges = g->n_edges;
   info->n_ranks = g->n_ranks;
-  info->max_out_degree = g->max_deg[1];
-  info->max_in_degree = g->max_deg[0];
+  if (g->maxdeg.p && g->n_edges > 0) {
+    unsigned long long md[2] = {0, 0};
+    TM_CUDA(cudaSetDevice(g->device));
+    TM_CUDA(cudaMemcpyAsync(md, g->maxdeg.p, 16, cudaMemcpyDeviceToHost, g->stream));
+    TM_CUDA(cudaStreamSynchronize(g->stream));
+    info->max_out_degree = (int64_t)md[1];
+    info->max_in_degree = (int64_t)md[0];
+  }
   info->n_selfloops = g->n_selfloops;
   info->device_bytes = g->device_bytes;
   info->device = g->device;
@@ -435,11 +464,17 @@ extern "C" int tm_graph_export_csr(const tm_graph *g, int dir, int64_t *indptr, 
 extern "C" void tm_graph_free(tm_graph *g) {
   if (!g) return;
   cudaSetDevice(g->device);
-  if (g->stream) cudaStreamSynchronize(g->stream);
+  cudaDeviceSynchronize();  // kernels on user streams may still read the graph
   bool own = g->owns_stream;
   cudaStream_t s = g->stream;
   for (int i = 0; i < 3; ++i)
     if (g->ev[i]) cudaEventDestroy(g->ev[i]);
+  for (int i = 0; i < 4; ++i)
+    if (g->piece_ev[i]) cudaEventDestroy(g->piece_ev[i]);
+  if (g->copy_stream) {
+    cudaStreamSynchronize(g->copy_stream);
+    cudaStreamDestroy(g->copy_stream);
+  }
 
   delete g;  // DevBuf destructors free device memory
   if (own && s) cudaStreamDestroy(s);

@@ -119,13 +119,20 @@ void count_launch(int n = 1);
 struct DevBuf {
   void *p = nullptr;
   size_t bytes = 0;
+  cudaStream_t pool_stream = nullptr;  // set: stream-ordered (memory pool) allocation
+  bool pooled = false;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) cudaFreeAsync(p, pool_stream);
+      else cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
+    pooled = false;
   }
-  int ensure(size_t n);  // grow-only
+  int ensure(size_t n);                     // grow-only, cudaMalloc
+  int ensure_on(size_t n, cudaStream_t s);  // grow-only, cudaMallocAsync on s (pool)
   template <class T> T *as() const { return static_cast<T *>(p); }
 };
 
@@ -164,7 +171,7 @@ struct tm_graph {
   int rank_bits = 0, node_bits = 0;
   int64_t device_bytes = 0;
 
-  tmb::DevBuf e_src, e_dst, e_rank, uniq_time, loop;
+  tmb::DevBuf e_src, e_dst, e_rank, uniq_time, loop, maxdeg;
   tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2];
 
   // mining scratch (grow-only)
@@ -173,6 +180,10 @@ struct tm_graph {
   tm_mine_stats last{};
   bool prof = false, prof_pending = false;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // host-output pieces: D2H of piece i overlaps mining of piece i+1
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t piece_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  tmb::DevBuf split_counts;
 
   tmb::DevGraph dev() const;
 };

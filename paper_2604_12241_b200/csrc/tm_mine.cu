@@ -53,6 +53,7 @@ constexpr int kDomSplit = 256;       // a trigger slice above this becomes domai
 constexpr int kDeepSplit = 64;       // chain nodes with wider windows become chain tasks
 constexpr int kTaskSpan = 128;       // entries per task (4 per lane)
 constexpr int kLvlDomU = 8, kLvlDomV = 9;  // Task::level of domain tasks
+constexpr int kHostPieces = 4;     // host-output pieces overlapped with their D2H
 
 struct Win {
   int a, b;
@@ -713,37 +714,64 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   Queue qb{g->tasks.as<Task>() + task_cap, cnt + 2, (int32_t)task_cap};
 
   const DevGraph dg = g->dev();
-  g->prof_pending = g->prof;
-  if (g->prof) TM_CUDA(cudaEventRecord(g->ev[0], s));
   const size_t smem = sizeof(long long) * kThreads * n_plans;
   if (smem > 48 * 1024)
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_mine_warp<<<grid_for(rows, kThreads), kThreads, smem, s>>>(
-      dg, dp, lo, rows, d_out, qa, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
-      (int32_t)split_cap);
-  TM_LAUNCHED("k_mine_warp");
-  if (g->prof) TM_CUDA(cudaEventRecord(g->ev[1], s));
-  const int task_grid = 148 * (2048 / kTaskThreads);
-  for (int r = 0; r < rounds; ++r) {
-    TM_CUDA(cudaMemsetAsync(qb.count, 0, sizeof(int32_t), s));
-    k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dp, lo, d_out, g->split_scratch.as<int32_t>(),
-                                                    qa, qb);
-    TM_LAUNCHED("k_mine_tasks");
-    std::swap(qa, qb);
+  // Host output: mine the range in pieces and copy each finished piece back
+  // on a copy stream while the next piece is mined — the D2H of the int64
+  // block (8*C bytes per trigger over PCIe) is the largest end-to-end cost.
+  const int pieces = (!out_on_device && rows >= (1 << 20)) ? kHostPieces : 1;
+  if (pieces > 1 && !g->copy_stream) {
+    TM_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < kHostPieces; ++i)
+      TM_CUDA(cudaEventCreateWithFlags(&g->piece_ev[i], cudaEventDisableTiming));
   }
-  if (rounds > 0) {
-    k_mine_finalize<<<148, 256, 0, s>>>(dp, d_out, g->heavy_q.as<int32_t>(), cnt,
-                                        g->split_scratch.as<int32_t>(), (int32_t)split_cap);
-    TM_LAUNCHED("k_mine_finalize");
+  if ((rc = g->split_counts.ensure(sizeof(int32_t) * kHostPieces))) return rc;
+  int32_t *piece_split = g->split_counts.as<int32_t>();
+  g->prof_pending = g->prof;
+  if (g->prof) TM_CUDA(cudaEventRecord(g->ev[0], s));
+  const int task_grid = 148 * (2048 / kTaskThreads);
+  const int64_t per = (rows + pieces - 1) / pieces;
+  for (int pc = 0; pc < pieces; ++pc) {
+    const int64_t r0 = std::min<int64_t>(rows, pc * per), r1 = std::min<int64_t>(rows, r0 + per);
+    long long *po = d_out + r0 * n_plans;
+    Queue a = qa, b = qb;
+    TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
+    k_mine_warp<<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
+        dg, dp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt,
+        g->split_scratch.as<int32_t>(), (int32_t)split_cap);
+    TM_LAUNCHED("k_mine_warp");
+    if (g->prof && pc == pieces - 1) TM_CUDA(cudaEventRecord(g->ev[1], s));
+    for (int r = 0; r < rounds; ++r) {
+      TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int32_t), s));
+      k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dp, lo + r0, po,
+                                                      g->split_scratch.as<int32_t>(), a, b);
+      TM_LAUNCHED("k_mine_tasks");
+      std::swap(a, b);
+    }
+    if (rounds > 0) {
+      k_mine_finalize<<<148, 256, 0, s>>>(dp, po, g->heavy_q.as<int32_t>(), cnt,
+                                          g->split_scratch.as<int32_t>(), (int32_t)split_cap);
+      TM_LAUNCHED("k_mine_finalize");
+    }
+    TM_CUDA(cudaMemcpyAsync(piece_split + pc, cnt, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (pieces > 1) {
+      TM_CUDA(cudaEventRecord(g->piece_ev[pc], s));
+      TM_CUDA(cudaStreamWaitEvent(g->copy_stream, g->piece_ev[pc], 0));
+      TM_CUDA(cudaMemcpyAsync(out + r0 * n_plans, po, sizeof(long long) * (size_t)(r1 - r0) * n_plans,
+                              cudaMemcpyDeviceToHost, g->copy_stream));
+    }
   }
   if (g->prof) TM_CUDA(cudaEventRecord(g->ev[2], s));
   if (!out_on_device) {
-    TM_CUDA(cudaMemcpyAsync(out, d_out, sizeof(long long) * (size_t)rows * n_plans,
-                            cudaMemcpyDeviceToHost, s));
-    int32_t nh = 0;
-    TM_CUDA(cudaMemcpyAsync(&nh, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (pieces == 1)
+      TM_CUDA(cudaMemcpyAsync(out, d_out, sizeof(long long) * (size_t)rows * n_plans,
+                              cudaMemcpyDeviceToHost, s));
+    int32_t ns[kHostPieces] = {0, 0, 0, 0};
+    TM_CUDA(cudaMemcpyAsync(ns, piece_split, sizeof(int32_t) * pieces, cudaMemcpyDeviceToHost, s));
+    if (pieces > 1) TM_CUDA(cudaStreamSynchronize(g->copy_stream));
     TM_CUDA(cudaStreamSynchronize(s));
-    g->last.heavy_triggers = nh;
+    g->last.heavy_triggers = (int64_t)ns[0] + ns[1] + ns[2] + ns[3];
   } else {
     g->last.heavy_triggers = -1;  // not read back on the async path
   }

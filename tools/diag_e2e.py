@@ -1,0 +1,29 @@
+"""End-to-end phase timing through the public API (GPU box):
+python tools/diag_e2e.py [hi-small]"""
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2604_12241_b200 as tmb  # noqa: E402
+from paper_2604_12241_b200 import synth  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "hi-small"
+g0 = synth.time_ordered(synth.generate(synth.CONFIGS[name]))
+pin = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).pin_memory().numpy()
+hs, hd, ht = pin(g0.src), pin(g0.dst), pin(g0.time)
+descs = [tmb.lower_plan(p) for p in tmb.full_pattern_set(86400)]
+hout = torch.empty((g0.edge_count, len(descs)), dtype=torch.int64).pin_memory().numpy()
+for rep in range(4):
+    t0 = time.perf_counter()
+    g = tmb.DeviceGraph(hs, hd, ht, node_count=g0.node_count)
+    t1 = time.perf_counter()
+    tmb.mine_rows(g, descs, 0, g.edge_count, out=hout)
+    t2 = time.perf_counter()
+    g.free()
+    t3 = time.perf_counter()
+    print(f"rep {rep}: build {1e3*(t1-t0):7.2f} ms  mine+D2H {1e3*(t2-t1):7.2f} ms  free {1e3*(t3-t2):6.2f} ms  "
+          f"total {1e3*(t3-t0):7.2f} ms", flush=True)
