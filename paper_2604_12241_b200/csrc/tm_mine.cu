@@ -89,20 +89,74 @@ struct Ctx {
   Win wui, wuo, wvi, wvo;  // trigger windows (u-in, u-out, v-in, v-out)
 };
 
+// Both variants measured slower on HI-Small (4.73 -> 5.25 ms/step,
+// tools/sweep_budget.py A/B): kept off, selectable for other graphs.
+#ifndef TM_UB_GALLOP
+#define TM_UB_GALLOP 0
+#endif
+#ifndef TM_FILL_INTERLEAVE
+#define TM_FILL_INTERLEAVE 0
+#endif
+
+// first index in [s, e) with r > x, galloping forward from s: windows are
+// short, so this is usually one load of a line the lower bound just touched
+__device__ __forceinline__ int ub_gallop(const uint32_t *__restrict__ r, int s, int e, uint32_t x) {
+  if (s >= e || __ldg(r + s) > x) return s;
+  int lo = s, step = 1;  // r[lo] <= x
+  while (lo + step < e && __ldg(r + lo + step) <= x) {
+    lo += step;
+    step <<= 1;
+  }
+  return ub_u32(r, lo + 1, min(lo + step, e), x);
+}
+
 // windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
 __device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
   const int a = __ldg(c.g.ptr[dir] + x), b = __ldg(c.g.ptr[dir] + x + 1);
   const int wa = lb_u32(c.g.rnk[dir], a, b, c.lo);
+#if TM_UB_GALLOP
+  return {wa, ub_gallop(c.g.rnk[dir], wa, b, c.hi)};
+#else
   return {wa, ub_u32(c.g.rnk[dir], wa, b, c.hi)};
+#endif
 }
 
-// trigger windows a delta group needs (bits: 1 u-in, 2 u-out, 4 v-in, 8 v-out)
+// trigger windows a delta group needs (bits: 1 u-in, 2 u-out, 4 v-in, 8 v-out).
+// The four lower-bound bisections run interleaved, so their dependent load
+// chains overlap (4 loads in flight per thread instead of 1).
 __device__ __forceinline__ void fill_windows(Ctx &c, int need) {
+#if !TM_FILL_INTERLEAVE
   c.wui = c.wuo = c.wvi = c.wvo = Win{0, 0};
   if (need & 1) c.wui = window(c, 0, c.u);
   if (need & 2) c.wuo = window(c, 1, c.u);
   if (need & 4) c.wvi = window(c, 0, c.v);
   if (need & 8) c.wvo = window(c, 1, c.v);
+  return;
+#endif
+  int a[4], b[4], e[4];
+  const uint32_t *r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int dir = i & 1, x = (i >> 1) ? c.v : c.u;
+    r[i] = c.g.rnk[dir];
+    const bool on = (need >> i) & 1;
+    a[i] = on ? __ldg(c.g.ptr[dir] + x) : 0;
+    b[i] = on ? __ldg(c.g.ptr[dir] + x + 1) : 0;
+    e[i] = b[i];
+  }
+  while (a[0] < b[0] || a[1] < b[1] || a[2] < b[2] || a[3] < b[3]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (a[i] < b[i]) {
+        const int m = (a[i] + b[i]) >> 1;
+        if (__ldg(r[i] + m) < c.lo) a[i] = m + 1; else b[i] = m;
+      }
+    }
+  }
+  c.wui = Win{a[0], ub_gallop(r[0], a[0], e[0], c.hi)};
+  c.wuo = Win{a[1], ub_gallop(r[1], a[1], e[1], c.hi)};
+  c.wvi = Win{a[2], ub_gallop(r[2], a[2], e[2], c.hi)};
+  c.wvo = Win{a[3], ub_gallop(r[3], a[3], e[3], c.hi)};
 }
 
 // self-loops of x inside the window (kernels.py:279-287): pair run (x, x)
@@ -404,7 +458,10 @@ __device__ __forceinline__ void flat_for(WarpShared &ws, int lane, int len, F &&
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kThreads) k_mine_warp(
+#ifndef TM_WARP_MINB  // min resident blocks per SM for k_mine_warp (register cap)
+#define TM_WARP_MINB 8  // 64 registers: measured best (profiles/ncu_r01_*)
+#endif
+__global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     int64_t n_rows, long long *__restrict__ out, Queue qu, int32_t *__restrict__ split_rows,
     int32_t *__restrict__ split_n, int32_t *__restrict__ scratch, int32_t split_cap) {
@@ -524,7 +581,7 @@ struct GlobalSink {  // contributions of one task item, straight to global memor
   __device__ __forceinline__ void c3() { atomicAdd(scr + 2, 1); }
 };
 
-__global__ void __launch_bounds__(kTaskThreads) k_mine_tasks(
+__global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next) {
   const int n = min(*in.count, in.cap);
@@ -720,7 +777,15 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   // Host output: mine the range in pieces and copy each finished piece back
   // on a copy stream while the next piece is mined — the D2H of the int64
   // block (8*C bytes per trigger over PCIe) is the largest end-to-end cost.
-  const int pieces = (!out_on_device && rows >= (1 << 20)) ? kHostPieces : 1;
+  // Only for page-locked output: a D2H into pageable memory blocks the host
+  // thread, which would serialize the pieces instead of overlapping them.
+  bool pinned = false;
+  if (!out_on_device) {
+    cudaPointerAttributes pa{};
+    pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+  }
+  const int pieces = (pinned && rows >= (1 << 20)) ? kHostPieces : 1;
   if (pieces > 1 && !g->copy_stream) {
     TM_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     for (int i = 0; i < kHostPieces; ++i)
