@@ -290,7 +290,7 @@ def main():
     b_edge = 16 + 24 + 8 * C + 8 * (g0.node_count + 1) / E
     rows = hi - lo
     lm, hm = float(np.mean(light_ms)), float(np.mean(heavy_ms))
-    dom_name, dom_ms = ("k_mine_light", lm) if lm >= hm else ("k_mine_heavy", hm)
+    dom_name, dom_ms = ("k_mine_warp", lm) if lm >= hm else ("k_mine_tasks+finalize", hm)
     achieved = rows * b_edge / (dom_ms / 1e3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
@@ -301,7 +301,7 @@ def main():
             traffic = ent.get("dram_bytes")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
-                "kernel_ms": dom_ms, "light_ms": lm, "heavy_ms": hm,
+                "kernel_ms": dom_ms, "warp_kernel_ms": lm, "task_kernels_ms": hm,
                 "bytes_per_edge": b_edge, "peak_source": peak_src,
                 "step_frac": E * b_edge / (ms_per_step / 1e3) / 1e9 / peak,
                 "model": "compulsory bytes per trigger = 16 (src,dst,t) + 24 (one out + one in CSR "
