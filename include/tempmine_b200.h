@@ -18,6 +18,9 @@
  *                        batch_scatter_gather :348, batch_stack :379; and the
  *                        generic-interpreter families cycle_5..8 / gs_count
  *                        (engine.py:516-562 on SURVEY.md Appendix B DSL)
+ *   tm_mine_members      the same dispatch with attribution = "members":
+ *                        engine.py:629-640 over _EmissionState instances
+ *                        engine.py:433-513
  *   tm_last_error        Python exceptions EngineInvariantError /
  *                        ValueError (engine.py:33,589,669-670)
  *
@@ -134,6 +137,15 @@ int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int
 
 /* Stats of the last tm_mine; with profiling on this waits for that call's
  * kernels to finish and fills the event timings. */
+/* Members attribution (engine.py:629-640, pattern_grammar.md:116-122):
+ * every instance found at a trigger in [lo, hi) that has the trigger as its
+ * temporally last member adds 1 to the row of EVERY member edge, so `out`
+ * is the full (n_edges x n_plans) block (C order).
+ * out_on_device = 1: contributions are ADDED into out (enqueued on stream);
+ *                 0: host out is overwritten with this range's block. */
+int tm_mine_members(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
+                    int64_t *out, int out_on_device, void *stream);
+
 int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats);
 
 /* on = 1: bracket the mining kernels of every tm_mine with CUDA events on

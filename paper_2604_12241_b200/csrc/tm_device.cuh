@@ -1,0 +1,158 @@
+// tm_device.cuh — device-side set primitives shared by the mining kernels
+// (tm_mine.cu: trigger attribution, tm_members.cu: members attribution).
+// See tm_internal.cuh for the graph layout they read.
+#pragma once
+
+#include "tm_internal.cuh"
+
+namespace tmb {
+namespace dev {
+
+struct Win {
+  int a, b;
+  __device__ __forceinline__ int len() const { return b - a; }
+};
+
+__device__ __forceinline__ int lb_u32(const uint32_t *__restrict__ r, int a, int b, uint32_t x) {
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (__ldg(r + m) < x) a = m + 1; else b = m;
+  }
+  return a;
+}
+__device__ __forceinline__ int ub_u32(const uint32_t *__restrict__ r, int a, int b, uint32_t x) {
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (__ldg(r + m) <= x) a = m + 1; else b = m;
+  }
+  return a;
+}
+__device__ __forceinline__ int lb_u64(const uint64_t *__restrict__ k, int a, int b, uint64_t x) {
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (__ldg(k + m) < x) a = m + 1; else b = m;
+  }
+  return a;
+}
+
+struct Ctx {
+  const DevGraph &g;  // a __grid_constant__ kernel parameter
+  int u, v;
+  uint32_t lo, hi;    // window in rank space
+  Win wui, wuo, wvi, wvo;  // trigger windows (u-in, u-out, v-in, v-out)
+};
+
+// Both variants measured slower on HI-Small (4.73 -> 5.25 ms/step,
+// tools/sweep_budget.py A/B): kept off, selectable for other graphs.
+#ifndef TM_UB_GALLOP
+#define TM_UB_GALLOP 0
+#endif
+#ifndef TM_FILL_INTERLEAVE
+#define TM_FILL_INTERLEAVE 0
+#endif
+
+// first index in [s, e) with r > x, galloping forward from s: windows are
+// short, so this is usually one load of a line the lower bound just touched
+__device__ __forceinline__ int ub_gallop(const uint32_t *__restrict__ r, int s, int e, uint32_t x) {
+  if (s >= e || __ldg(r + s) > x) return s;
+  int lo = s, step = 1;  // r[lo] <= x
+  while (lo + step < e && __ldg(r + lo + step) <= x) {
+    lo += step;
+    step <<= 1;
+  }
+  return ub_u32(r, lo + 1, min(lo + step, e), x);
+}
+
+// windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
+__device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
+  const int a = __ldg(c.g.ptr[dir] + x), b = __ldg(c.g.ptr[dir] + x + 1);
+  const int wa = lb_u32(c.g.rnk[dir], a, b, c.lo);
+#if TM_UB_GALLOP
+  return {wa, ub_gallop(c.g.rnk[dir], wa, b, c.hi)};
+#else
+  return {wa, ub_u32(c.g.rnk[dir], wa, b, c.hi)};
+#endif
+}
+
+// trigger windows a delta group needs (bits: 1 u-in, 2 u-out, 4 v-in, 8 v-out).
+// The four lower-bound bisections run interleaved, so their dependent load
+// chains overlap (4 loads in flight per thread instead of 1).
+__device__ __forceinline__ void fill_windows(Ctx &c, int need) {
+#if !TM_FILL_INTERLEAVE
+  c.wui = c.wuo = c.wvi = c.wvo = Win{0, 0};
+  if (need & 1) c.wui = window(c, 0, c.u);
+  if (need & 2) c.wuo = window(c, 1, c.u);
+  if (need & 4) c.wvi = window(c, 0, c.v);
+  if (need & 8) c.wvo = window(c, 1, c.v);
+#else
+  int a[4], b[4], e[4];
+  const uint32_t *r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int dir = i & 1, x = (i >> 1) ? c.v : c.u;
+    r[i] = c.g.rnk[dir];
+    const bool on = (need >> i) & 1;
+    a[i] = on ? __ldg(c.g.ptr[dir] + x) : 0;
+    b[i] = on ? __ldg(c.g.ptr[dir] + x + 1) : 0;
+    e[i] = b[i];
+  }
+  while (a[0] < b[0] || a[1] < b[1] || a[2] < b[2] || a[3] < b[3]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (a[i] < b[i]) {
+        const int m = (a[i] + b[i]) >> 1;
+        if (__ldg(r[i] + m) < c.lo) a[i] = m + 1; else b[i] = m;
+      }
+    }
+  }
+  c.wui = Win{a[0], ub_gallop(r[0], a[0], e[0], c.hi)};
+  c.wuo = Win{a[1], ub_gallop(r[1], a[1], e[1], c.hi)};
+  c.wvi = Win{a[2], ub_gallop(r[2], a[2], e[2], c.hi)};
+  c.wvo = Win{a[3], ub_gallop(r[3], a[3], e[3], c.hi)};
+#endif
+}
+
+// self-loops of x inside the window (kernels.py:279-287): pair run (x, x)
+__device__ __forceinline__ int loops_in_window(const Ctx &c, int x) {
+  if (!__ldg(c.g.loop + x)) return 0;
+  const int a = __ldg(c.g.ptr[1] + x), b = __ldg(c.g.ptr[1] + x + 1);
+  const uint64_t base = (uint64_t)(uint32_t)x << c.g.rank_bits;
+  return lb_u64(c.g.pkey[1], a, b, base + c.hi + 1) - lb_u64(c.g.pkey[1], a, b, base + c.lo);
+}
+
+// CSR entry j is the first occurrence of its neighbour inside the window
+// (np.unique, kernels.py:59): the previous entry with the same (owner, nbr)
+// lies before lo (prev = rank + 1, 0 = none)
+__device__ __forceinline__ bool first_in_window(const Ctx &c, int dir, int j) {
+  return __ldg(c.g.prev[dir] + j) <= c.lo;
+}
+
+// does x's dir-window w contain neighbour n?  Windows are time-local and
+// short: scan them.  A wide w (a hub) is answered by one bisection of the
+// SHORTER pair run: x's dir run keyed by n, or n's opposite run keyed by x
+// (n in N^dir(x)  <=>  x in N^{1-dir}(n)).
+constexpr int kScanWin = 16;
+__device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
+  if (w.len() <= kScanWin) {
+    bool hit = false;
+    for (int j = w.a; j < w.b && !hit; ++j) hit = __ldg(c.g.nbr[dir] + j) == n;
+    return hit;
+  }
+  const int xs = __ldg(c.g.ptr[dir] + x), xe = __ldg(c.g.ptr[dir] + x + 1);
+  const int ns = __ldg(c.g.ptr[dir ^ 1] + n), ne = __ldg(c.g.ptr[dir ^ 1] + n + 1);
+  const bool from_x = xe - xs <= ne - ns;
+  const uint64_t *k = c.g.pkey[from_x ? dir : dir ^ 1];
+  const int s = from_x ? xs : ns, e = from_x ? xe : ne;
+  const uint64_t base = (uint64_t)(uint32_t)(from_x ? n : x) << c.g.rank_bits;
+  const int q = lb_u64(k, s, e, base + c.lo);
+  return q < e && __ldg(k + q) <= base + c.hi;
+}
+
+__device__ __forceinline__ long long warp_sum(long long x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+}  // namespace dev
+}  // namespace tmb

@@ -124,12 +124,14 @@ __global__ void k_indptr(const uint64_t *__restrict__ keys, int64_t n, int shift
 // neighbour: prev[p] = its rank + 1 (0 = none)
 __global__ void k_pair_fill(const uint64_t *__restrict__ pair_sorted, const uint32_t *__restrict__ pids,
                             const int32_t *__restrict__ nbr, const uint32_t *__restrict__ rnk,
-                            int64_t n, int rbits, uint64_t *__restrict__ pkey,
-                            uint32_t *__restrict__ prev) {
+                            const int32_t *__restrict__ eid, int64_t n, int rbits,
+                            uint64_t *__restrict__ pkey, uint32_t *__restrict__ prev,
+                            int32_t *__restrict__ peid) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const uint32_t p = pids[q];
   pkey[q] = ((uint64_t)(uint32_t)nbr[p] << rbits) | rnk[p];
+  peid[q] = eid[p];
   prev[p] = (q > 0 && pair_sorted[q - 1] == pair_sorted[q]) ? rnk[pids[q - 1]] + 1u : 0u;
 }
 
@@ -199,6 +201,8 @@ tmb::DevGraph tm_graph::dev() const {
     g.rnk[d] = rnk[d].as<uint32_t>();
     g.pkey[d] = pkey[d].as<uint64_t>();
     g.prev[d] = prev[d].as<uint32_t>();
+    g.eid[d] = eid[d].as<int32_t>();
+    g.peid[d] = peid[d].as<int32_t>();
   }
   g.loop = loop.as<uint8_t>();
   return g;
@@ -235,7 +239,8 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
   for (int d = 0; d < 2; ++d) {
     if ((rc = g->ptr[d].ensure_on(4 * (N + 1), s)) || (rc = g->nbr[d].ensure_on(4 * Ea, s)) ||
         (rc = g->rnk[d].ensure_on(4 * Ea, s)) || (rc = g->eid[d].ensure_on(4 * Ea, s)) ||
-        (rc = g->pkey[d].ensure_on(8 * Ea, s)) || (rc = g->prev[d].ensure_on(4 * Ea, s)))
+        (rc = g->pkey[d].ensure_on(8 * Ea, s)) || (rc = g->prev[d].ensure_on(4 * Ea, s)) ||
+        (rc = g->peid[d].ensure_on(4 * Ea, s)))
       return rc;
   }
   if (E == 0) {
@@ -329,8 +334,9 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
     uint32_t *pv2 = (pv == va.as<uint32_t>()) ? vb.as<uint32_t>() : va.as<uint32_t>();
     if ((rc = radix_sort_pairs(pk, pv, pk2, pv2, E, 2 * g->node_bits, s, &ps, &pvs))) return rc;
     k_pair_fill<<<grid_for(E, kB), kB, 0, s>>>(ps, pvs, g->nbr[d].as<int32_t>(),
-                                               g->rnk[d].as<uint32_t>(), E, g->rank_bits,
-                                               g->pkey[d].as<uint64_t>(), g->prev[d].as<uint32_t>());
+                                               g->rnk[d].as<uint32_t>(), g->eid[d].as<int32_t>(), E,
+                                               g->rank_bits, g->pkey[d].as<uint64_t>(),
+                                               g->prev[d].as<uint32_t>(), g->peid[d].as<int32_t>());
     TM_LAUNCHED("k_pair_fill");
     unsigned long long *md = g->maxdeg.as<unsigned long long>() + d;  // read lazily by info
     TM_CUDA(cudaMemsetAsync(md, 0, 8, s));
@@ -385,7 +391,7 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
   for (const DevBuf *b : {&g->e_src, &g->e_dst, &g->e_rank, &g->uniq_time, &g->loop})
     bytes += (int64_t)b->bytes;
   for (int d = 0; d < 2; ++d)
-    for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d]})
+    for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d], &g->peid[d]})
       bytes += (int64_t)b->bytes;
   g->device_bytes = bytes;
   *out = g;

@@ -49,6 +49,8 @@ struct DevGraph {
   const uint32_t *rnk[2];
   const uint64_t *pkey[2];
   const uint32_t *prev[2];
+  const int32_t *eid[2];   // edge id per CSR slot (members attribution)
+  const int32_t *peid[2];  // edge id per pair slot (members attribution)
   const uint8_t *loop;
 };
 
@@ -172,7 +174,7 @@ struct tm_graph {
   int64_t device_bytes = 0;
 
   tmb::DevBuf e_src, e_dst, e_rank, uniq_time, loop, maxdeg;
-  tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2];
+  tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2], peid[2];
 
   // mining scratch (grow-only)
   tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks, split_scratch;

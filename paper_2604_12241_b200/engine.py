@@ -5,10 +5,12 @@ errors (EngineInvariantError for duplicate names / slot mismatch, ValueError
 for workers < 1), same return type (FeatureMatrix, engine.py:55-103).  The
 work runs in libtempmine_b200.so on one GPU; `workers` is accepted for API
 compatibility (the reference's fork-pool width) and has no effect — the
-whole trigger range is one launch, balanced on the device.  Paths the GPU
-does not implement (members attribution, instance collection, arbitrary
-GENERIC stage programs) raise UnsupportedPlanError instead of silently
-falling back to a CPU interpreter.
+whole trigger range is one launch, balanced on the device.  Columns with
+attribution "members" go through tm_mine_members (full-matrix
+contributions, engine.py:629-640).  Paths the GPU does not implement
+(instance collection, arbitrary GENERIC stage programs) raise
+UnsupportedPlanError instead of silently falling back to a CPU
+interpreter.
 """
 
 from __future__ import annotations
@@ -112,10 +114,28 @@ def lower_all(plans: list) -> tuple[list, list[PlanDesc]]:
     return plans, descs
 
 
+def mine_members(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int = 0, hi: int | None = None,
+                 out: np.ndarray | None = None) -> np.ndarray:
+    """Members attribution of triggers [lo, hi): full (n_edges, len(descs)) block
+    (engine.py:629-640) — every counted instance adds 1 to each member row."""
+    hi = dgraph.edge_count if hi is None else hi
+    if out is None:
+        out = np.empty((dgraph.edge_count, len(descs)), dtype=np.int64)
+    if not descs or dgraph.edge_count == 0:
+        out[:] = 0
+        return out
+    arr = _lib.plan_array(descs)
+    rc = _lib.load().tm_mine_members(dgraph.handle, arr, len(descs), lo, hi, _lib.ptr(out), 0, None)
+    _lib.check(rc, "tm_mine_members")
+    return out
+
+
 def mine_rows(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int,
               out: np.ndarray | None = None) -> np.ndarray:
     """Rows [lo, hi) x len(descs) into a host int64 array (C order)."""
     rows = hi - lo
+    if any(d.members for d in descs):
+        raise ValueError("mine_rows takes trigger-attribution columns; use mine_members")
     if out is None:
         out = np.empty((rows, len(descs)), dtype=np.int64)
     if rows == 0 or not descs:
@@ -153,13 +173,21 @@ def mine(graph, plans, workers: int = 1, collect_instances: bool = False, *, dev
     """
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
-    if collect_instances:
+    if collect_instances:  # instance records are a separate §8f row
         raise _lib.UnsupportedPlanError(
             _lib.TM_E_UNSUPPORTED_PLAN,
             "collect_instances=True needs per-instance records, which the GPU path does not emit")
     plans, descs = lower_all(plans)
     dg = as_device_graph(graph, device)
-    values = mine_rows(dg, descs, 0, dg.edge_count)
+    trig = [i for i, d in enumerate(descs) if not d.members]
+    memb = [i for i, d in enumerate(descs) if d.members]
+    if not memb:
+        values = mine_rows(dg, descs, 0, dg.edge_count)
+    else:
+        values = np.empty((dg.edge_count, len(descs)), dtype=np.int64)
+        if trig:
+            values[:, trig] = mine_rows(dg, [descs[i] for i in trig], 0, dg.edge_count)
+        values[:, memb] = mine_members(dg, [descs[i] for i in memb])
     label = getattr(graph, "edge_label", None)
     if label is None:
         label = dg.edge_label

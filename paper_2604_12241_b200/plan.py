@@ -122,6 +122,7 @@ class PlanDesc:
     cycle_len: int = 0
     min_size: int = 1
     delta: int = 0
+    members: bool = False  # attribution "members" -> tm_mine_members (not a C field)
 
 
 # ---------------------------------------------------------------------------
@@ -332,10 +333,16 @@ def recognize(plan) -> str | None:
 
 def lower_plan(plan) -> PlanDesc:
     """ExecutionPlan (reference or ours) -> PlanDesc; raises UnsupportedPlanError."""
+    import dataclasses
     name = getattr(plan, "name", "?")
-    if getattr(plan, "attribution", "trigger") != "trigger":
-        raise UnsupportedPlanError(
-            TM_E_UNSUPPORTED_PLAN, f"plan {name}: members attribution is not on the GPU path")
+    attribution = getattr(plan, "attribution", "trigger")
+    if attribution not in ("trigger", "members"):
+        raise UnsupportedPlanError(TM_E_UNSUPPORTED_PLAN, f"plan {name}: unknown attribution {attribution!r}")
+    desc = _lower_trigger(plan, name)
+    return dataclasses.replace(desc, members=True) if attribution == "members" else desc
+
+
+def _lower_trigger(plan, name) -> PlanDesc:
     delta = int(plan.delta)
     if delta < 0:
         raise ValueError(f"plan {name}: delta must be non-negative")

@@ -95,9 +95,9 @@ def gs_text(delta: int, min_size: int = 2, name: str = "gs_count") -> str:
 
 
 def builtin_with(name: str, delta: int, min_size: int | None = None,
-                 new_name: str | None = None) -> dsl.ValidatedPattern:
+                 new_name: str | None = None, attribution: str = "trigger") -> dsl.ValidatedPattern:
     vp = plan.load_builtin(name)
-    spec = dataclasses.replace(vp.spec, delta=delta)
+    spec = dataclasses.replace(vp.spec, delta=delta, attribution=attribution)
     if min_size is not None:
         spec = dataclasses.replace(spec, emit=dataclasses.replace(spec.emit, min_size=min_size))
     if new_name is not None:
@@ -105,11 +105,14 @@ def builtin_with(name: str, delta: int, min_size: int | None = None,
     return dsl.must_validate(spec)
 
 
-def ext_pattern(base: str, delta: int, min_size: int | None, name: str) -> dsl.ValidatedPattern:
+def ext_pattern(base: str, delta: int, min_size: int | None, name: str,
+                attribution: str = "trigger") -> dsl.ValidatedPattern:
     if base == "gs_count":
         text = gs_text(delta, 2 if min_size is None else min_size, name)
     else:
         text = cycle_k_text(int(base.split("_")[1]), delta, 1 if min_size is None else min_size, name)
+    if attribution != "trigger":
+        text = text.replace("\n\nstage:", f"\nattribution: {attribution}\n\nstage:", 1)
     return dsl.must_validate(dsl.parse_pattern(text))
 
 
@@ -126,18 +129,19 @@ VARIANT_SPECS = [("sg_k1", "sg_count", 1), ("sg_k3", "sg_count", 3),
 ALL_SPECS = BUILTIN_SPECS + EXT_SPECS + VARIANT_SPECS
 
 
-def patterns_for(specs, delta: int):
+def patterns_for(specs, delta: int, attribution: str = "trigger"):
     out = []
     for col, base, k in specs:
         if base in BUILTIN_COLUMNS:
-            out.append(builtin_with(base, delta, k, None if col == base else col))
+            out.append(builtin_with(base, delta, k, None if col == base else col, attribution))
         else:
-            out.append(ext_pattern(base, delta, k, col))
+            out.append(ext_pattern(base, delta, k, col, attribution))
     return out
 
 
-def mine_columns(g: TemporalGraph, specs, delta: int, workers: int = 1) -> np.ndarray:
-    pats = patterns_for(specs, delta)
+def mine_columns(g: TemporalGraph, specs, delta: int, workers: int = 1,
+                 attribution: str = "trigger") -> np.ndarray:
+    pats = patterns_for(specs, delta, attribution)
     plans = [compile_pattern(p, g.stats) for p in pats]
     fm = mine(g, plans, workers=workers)
     return np.stack([fm.column(col) for col, _, _ in specs], axis=1).astype(np.int64)
@@ -360,6 +364,49 @@ def make_cfg1():
 
 CUSTOM_DIR = Path("/root/reference/pkg/tests/data/custom")
 CUSTOM_NAMES = ("spray_union", "filtered_senders", "sg_ordered", "stack_forward", "chain_5cycle")
+
+
+# ---------------------------------------------------------------------------
+# members attribution (engine.py:629-640, pattern_grammar.md:116-122): an
+# instance is anchored at its temporally last member edge and adds 1 to the
+# row of every member edge
+
+
+def _corpus_one_members(p):
+    seed, n_nodes, n_edges, horizon, deltas = p
+    edges = corpus_records(seed, n_nodes, n_edges, horizon)
+    g = graph_from_edges(edges)
+    vals = [mine_columns(g, CORPUS_SPECS, d, attribution="members") for d in deltas]
+    return np.stack(vals)
+
+
+def make_members():
+    cases = []
+    for name, (edges, deltas) in HAND_GRAPHS.items():
+        g = graph_from_edges(edges)
+        for delta in deltas:
+            vals = mine_columns(g, ALL_SPECS, delta, attribution="members")
+            cases.append({"name": name, "edges": [list(e) for e in edges], "delta": delta,
+                          "values": vals.tolist()})
+    doc = {"generator": "tests/golden/make_golden.py", "reference": "tempmine 0.1.0 (engine.mine)",
+           "attribution": "members", "columns": spec_json(ALL_SPECS), "cases": cases}
+    (OUT / "hand_members.json").write_text(json.dumps(doc, separators=(",", ":")) + "\n")
+    print(f"hand_members.json: {len(cases)} cases")
+    params = corpus_params()
+    with multiprocessing.get_context("fork").Pool(os.cpu_count()) as pool:
+        res = pool.map(_corpus_one_members, params, chunksize=1)
+    vals = np.concatenate([r.transpose(1, 0, 2) for r in res])
+    assert vals.max() < 2 ** 31
+    np.savez_compressed(OUT / "corpus_members.npz", values=vals.astype(np.int32),
+                        columns=json.dumps(spec_json(CORPUS_SPECS)))
+    print("corpus_members.npz written (edges/deltas: corpus.npz)")
+    seed, n, e, h, deltas = TIES_CASES[0]
+    z = np.load(OUT / "ties.npz")
+    g = graph_from_arrays(z["src0"].astype(np.int64), z["dst0"].astype(np.int64), z["time0"].astype(np.int64))
+    tv = np.stack([mine_columns(g, ALL_SPECS, d, workers=os.cpu_count(), attribution="members")
+                   for d in deltas], axis=1)
+    np.savez_compressed(OUT / "ties_members.npz", values0=tv, columns=json.dumps(spec_json(ALL_SPECS)))
+    print("ties_members.npz written (case 0)")
 
 
 def make_plans():

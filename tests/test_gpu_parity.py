@@ -222,3 +222,64 @@ def test_single_timestamp_and_extreme_times(tmb):
         t = np.full(5, t0, dtype=np.int64)
         _oracle_vs_gpu(tmb, src, dst, t, 0)
         _oracle_vs_gpu(tmb, src, dst, t, 2**61)
+
+
+# ---------------------------------------------------------------- members
+
+def _mdescs(tmb, cols, delta):
+    import dataclasses
+    return [dataclasses.replace(d, members=True) for d in _descs(tmb, cols, delta)]
+
+
+def test_members_hand_cases(tmb):
+    doc = json.loads((GOLDEN / "hand_members.json").read_text())
+    for case in doc["cases"]:
+        e = np.array(case["edges"], dtype=np.int64)
+        g = tmb.DeviceGraph(e[:, 0], e[:, 1], e[:, 2])
+        got = tmb.mine_members(g, _mdescs(tmb, doc["columns"], case["delta"]))
+        g.free()
+        np.testing.assert_array_equal(got, np.array(case["values"]), err_msg=f"{case['name']} d={case['delta']}")
+
+
+def test_members_corpus(tmb):
+    zm = load_npz("corpus_members.npz")
+    cols = columns_of(zm)
+    vals_all = zm["values"].astype(np.int64)
+    off = load_npz("corpus.npz")["offsets"]
+    for i, edges, deltas, _ in corpus_graphs():
+        g = tmb.DeviceGraph(edges[:, 0], edges[:, 1], edges[:, 2])
+        for k, d in enumerate(deltas.tolist()):
+            got = tmb.mine_members(g, _mdescs(tmb, cols, d))
+            np.testing.assert_array_equal(got, vals_all[off[i]:off[i + 1], k, :], err_msg=f"graph {i} delta {d}")
+        g.free()
+
+
+def test_members_ties(tmb):
+    z = load_npz("ties.npz")
+    zm = load_npz("ties_members.npz")
+    meta = json.loads(str(z["meta"]))
+    cols = columns_of(zm)
+    g = tmb.DeviceGraph(z["src0"], z["dst0"], z["time0"])
+    for k, d in enumerate(meta[0]["deltas"]):
+        got = tmb.mine_members(g, _mdescs(tmb, cols, d))
+        np.testing.assert_array_equal(got, zm["values0"][:, k, :], err_msg=f"ties members delta {d}")
+    g.free()
+
+
+def test_mine_mixed_attribution(tmb):
+    """mine() with trigger and members columns in one call (engine.py:693-699)."""
+    import dataclasses
+    from types import SimpleNamespace
+    doc = json.loads((GOLDEN / "hand_members.json").read_text())
+    trig = load_hand()
+    case = next(c for c in doc["cases"] if c["name"] == "sg_planted" and c["delta"] == 10)
+    tcase = next(c for c in trig["cases"] if c["name"] == "sg_planted" and c["delta"] == 10)
+    e = np.array(case["edges"], dtype=np.int64)
+    g = SimpleNamespace(node_count=5, edge_src=e[:, 0], edge_dst=e[:, 1], edge_time=e[:, 2],
+                        edge_label=np.full(len(e), -1, np.int8))
+    sg_m = dataclasses.replace(tmb.builtin_plan("sg_count", 10), name="sg_m", attribution="members")
+    fm = tmb.mine(g, [sg_m, tmb.builtin_plan("sg_count", 10)])
+    names = [c["column"] for c in doc["columns"]]
+    j = names.index("sg_count")
+    assert fm.column("sg_m").tolist() == [r[j] for r in case["values"]]
+    assert fm.column("sg_count").tolist() == [r[j] for r in tcase["values"]]

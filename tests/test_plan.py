@@ -83,11 +83,14 @@ def test_unrecognized_custom_patterns_are_rejected(name):
         P.lower_plan(_obj(e["plan"]))
 
 
-def test_members_attribution_rejected():
+def test_members_attribution_lowering():
     import dataclasses
-    p = dataclasses.replace(P.builtin_plan("fan_in"), attribution="members")
+    p = dataclasses.replace(P.builtin_plan("sg_count"), attribution="members")
+    d = P.lower_plan(p)
+    assert d.members and d.family == 4 and d.min_size == 2
+    assert not P.lower_plan(P.builtin_plan("sg_count")).members
     with pytest.raises(UnsupportedPlanError):
-        P.lower_plan(p)
+        P.lower_plan(dataclasses.replace(p, attribution="edges"))
 
 
 def test_bad_parameters():
