@@ -259,6 +259,7 @@ __device__ __forceinline__ void v_item(const Ctx &c, const DevPlans &P, const De
 // ------------------------------------------------------------ k_mine_warp
 
 struct WarpShared {
+  int rowid[32];
   int u[32], v[32];
   uint32_t lo[32], hi[32];
   Win wui[32], wuo[32], wvi[32], wvo[32];
@@ -320,7 +321,8 @@ __device__ __forceinline__ void flat_for(WarpShared &ws, int lane, int len, F &&
 __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     int64_t n_rows, long long *__restrict__ out, Queue qu, int32_t *__restrict__ split_rows,
-    int32_t *__restrict__ split_n, int32_t *__restrict__ scratch, int32_t split_cap) {
+    int32_t *__restrict__ split_n, int32_t *__restrict__ scratch, int32_t split_cap,
+    const int32_t *__restrict__ order) {
   extern __shared__ long long stage_all[];  // [warp][32][C]
   __shared__ WarpShared wsh[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -328,8 +330,12 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
   const int C = P.n;
   long long *stage = stage_all + (size_t)warp * 32 * C;
   const int64_t wrow0 = (int64_t)blockIdx.x * kThreads + warp * 32;
-  const int64_t row = wrow0 + lane;
-  const bool valid = row < n_rows;
+  const int64_t pos = wrow0 + lane;  // position in processing order
+  const bool valid = pos < n_rows;
+  // trigger order: edge-id order, or (full range only) `order` = the
+  // out-CSR slots, so a warp's triggers share sources and their windows
+  const int64_t row = valid ? (order ? (int64_t)__ldg(order + pos) : pos) : pos;
+  ws.rowid[lane] = (int)row;
   int u = 0, v = 0;
   uint32_t r = 0;
   if (valid) {
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     flat_for(ws, lane, vlen, [&](int o, int k) {
       const Ctx co = ctx_of(g, ws, o);
       SmemSink sk{ws, stage, o, C};
-      v_item(co, P, gr, gi, (int)(wrow0 + o), co.wvo.a + k, sk, qu);
+      v_item(co, P, gr, gi, ws.rowid[o], co.wvo.a + k, sk, qu);
     });
     // whole-count columns: stack a * c (kernels.py:379-402), cycle_3 threshold
     if (valid) {
@@ -418,6 +424,11 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     __syncwarp();
   }
   __syncwarp();
+  if (order) {  // permuted rows: each lane writes its own
+    if (valid)
+      for (int i = 0; i < C; ++i) out[row * C + i] = stage[lane * C + i];
+    return;
+  }
   const int64_t left = n_rows - wrow0;
   const int nrow = left < 32 ? (int)(left > 0 ? left : 0) : 32;
   long long *dst = out + wrow0 * C;
@@ -518,6 +529,16 @@ __global__ void k_lo_table(const int64_t *__restrict__ uniq, int64_t R, long lon
 }  // namespace tmb
 
 using namespace tmb;
+
+// TM_ORDER=1 processes full-range calls in out-CSR (source) order; measured
+// neutral (HI-Small -3%, HI-Medium +2%), so edge-id order stays the default
+static bool source_order() {
+  static bool on = [] {
+    const char *e = getenv("TM_ORDER");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 
 extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
                        int64_t *out, int out_on_device, void *stream) {
@@ -658,9 +679,12 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     long long *po = d_out + r0 * n_plans;
     Queue a = qa, b = qb;
     TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
+    // full-range device-output calls process triggers in out-CSR order
+    const int32_t *order = (pieces == 1 && lo == 0 && hi == g->n_edges && source_order())
+                               ? g->eid[1].as<int32_t>() : nullptr;
     k_mine_warp<<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
         dg, dp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt,
-        g->split_scratch.as<int32_t>(), (int32_t)split_cap);
+        g->split_scratch.as<int32_t>(), (int32_t)split_cap, order);
     TM_LAUNCHED("k_mine_warp");
     if (g->prof && pc == pieces - 1) TM_CUDA(cudaEventRecord(g->ev[1], s));
     for (int r = 0; r < rounds; ++r) {

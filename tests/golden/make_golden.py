@@ -409,6 +409,17 @@ def make_members():
     print("ties_members.npz written (case 0)")
 
 
+def make_cfg1_members():
+    cfg = synth.SynthConfig(**CFG1, plants=CFG1_PLANTS)
+    records, _ = synth.generate(cfg)
+    g = build_graph(records)
+    specs = BUILTIN_SPECS + [("cycle_5", "cycle_5", None), ("gs_count", "gs_count", None)]
+    t0 = time.time()
+    vals = mine_columns(g, specs, 86400, workers=os.cpu_count(), attribution="members")
+    print(f"cfg1 members mined in {time.time() - t0:.1f}s")
+    np.savez_compressed(OUT / "cfg1_members.npz", values=vals, columns=json.dumps(spec_json(specs)))
+
+
 def make_plans():
     entries = []
     for col, base, k in ALL_SPECS:
