@@ -21,6 +21,8 @@
  *   tm_mine_members      the same dispatch with attribution = "members":
  *                        engine.py:629-640 over _EmissionState instances
  *                        engine.py:433-513
+ *   tm_csv_format /      FeatureMatrix.to_csv engine.py:73-103 (GPU int->text)
+ *   tm_csv_fetch
  *   tm_last_error        Python exceptions EngineInvariantError /
  *                        ValueError (engine.py:33,589,669-670)
  *
@@ -147,6 +149,16 @@ int tm_mine_members(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t
                     int64_t *out, int out_on_device, void *stream);
 
 int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats);
+
+/* Feature CSV rows (FeatureMatrix.to_csv, engine.py:73-103; header line not
+ * included): "edge_id,src,dst,timestamp,label,<features>\n" per edge, "%d"
+ * fields, empty label cell when labels is NULL or the label is negative.
+ * values: n_edges x n_cols int64 (host, or device when values_on_device);
+ * labels: host int8[n_edges] or NULL.  The text stays on the device;
+ * *out_bytes receives its length, tm_csv_fetch copies it out. */
+int tm_csv_format(tm_graph *g, const int64_t *values, int values_on_device, int n_cols,
+                  const int8_t *labels, int64_t *out_bytes);
+int tm_csv_fetch(tm_graph *g, char *dst, int64_t n_bytes);
 
 /* on = 1: bracket the mining kernels of every tm_mine with CUDA events on
  * the launch stream (read back by tm_last_mine_stats). */

@@ -64,6 +64,8 @@ SIGNATURES = {
     "tm_mine_members": (ctypes.c_int, [_P, ctypes.POINTER(TmPlanDesc), ctypes.c_int, ctypes.c_int64,
                                        ctypes.c_int64, _P, ctypes.c_int, _P]),
     "tm_last_mine_stats": (ctypes.c_int, [_P, ctypes.POINTER(TmMineStats)]),
+    "tm_csv_format": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(ctypes.c_int64)]),
+    "tm_csv_fetch": (ctypes.c_int, [_P, _P, ctypes.c_int64]),
     "tm_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
     "tm_kernel_launch_count": (ctypes.c_int64, []),
     "tm_last_error": (ctypes.c_char_p, []),

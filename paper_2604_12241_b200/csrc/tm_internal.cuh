@@ -178,6 +178,8 @@ struct tm_graph {
 
   // mining scratch (grow-only)
   tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks, split_scratch;
+  tmb::DevBuf csv_buf;  // formatted feature CSV (tm_csv_format)
+  int64_t csv_bytes = 0;
   int64_t lo_tab_cap = 0;
   tm_mine_stats last{};
   bool prof = false, prof_pending = false;

@@ -16,7 +16,7 @@ interpreter.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -39,6 +39,8 @@ class FeatureMatrix:
     edge_dst: np.ndarray
     edge_time: np.ndarray
     edge_label: np.ndarray
+    # the device graph these rows were mined on: to_csv formats on the GPU
+    device_graph: object = field(default=None, repr=False, compare=False)
 
     @property
     def edge_count(self) -> int:
@@ -49,7 +51,11 @@ class FeatureMatrix:
 
     def to_csv(self, path: str) -> None:
         """edge_id,src,dst,timestamp,label,<features> — byte-identical to the
-        reference writer (engine.py:73-103): empty label cell when < 0."""
+        reference writer (engine.py:73-103): empty label cell when < 0.
+        Rows are formatted on the GPU (tm_csv_format) when the matrix came
+        from a device graph, else on the host."""
+        if self.device_graph is not None:
+            return self._to_csv_gpu(path)
         n = self.edge_count
         with open(path, "w", encoding="utf-8", newline="\n") as fh:
             fh.write("edge_id,src,dst,timestamp,label")
@@ -74,6 +80,24 @@ class FeatureMatrix:
                     rows = np.char.add(np.char.add(rows, ","), c)
                 fh.write("\n".join(rows.tolist()))
                 fh.write("\n")
+
+
+    def _to_csv_gpu(self, path: str) -> None:
+        dg = self.device_graph
+        vals = np.ascontiguousarray(self.values, dtype=np.int64)
+        if vals.shape != (dg.edge_count, len(self.columns)):
+            raise ValueError("values do not match the device graph")
+        lab = np.ascontiguousarray(self.edge_label, dtype=np.int8)
+        n = ctypes.c_int64()
+        lib = _lib.load()
+        _lib.check(lib.tm_csv_format(dg.handle, _lib.ptr(vals), 0, vals.shape[1], _lib.ptr(lab),
+                                     ctypes.byref(n)), "tm_csv_format")
+        buf = np.empty(n.value, dtype=np.uint8)
+        _lib.check(lib.tm_csv_fetch(dg.handle, _lib.ptr(buf), n.value), "tm_csv_fetch")
+        with open(path, "wb") as fh:
+            fh.write(("edge_id,src,dst,timestamp,label" + "".join("," + c for c in self.columns)
+                      + "\n").encode("utf-8"))
+            fh.write(memoryview(buf))
 
 
 def merge_features(partials: list) -> FeatureMatrix:
@@ -193,4 +217,4 @@ def mine(graph, plans, workers: int = 1, collect_instances: bool = False, *, dev
         label = dg.edge_label
     return FeatureMatrix(columns=tuple(p.name for p in plans), values=values,
                          edge_src=graph.edge_src, edge_dst=graph.edge_dst,
-                         edge_time=graph.edge_time, edge_label=label)
+                         edge_time=graph.edge_time, edge_label=label, device_graph=dg)

@@ -283,3 +283,30 @@ def test_mine_mixed_attribution(tmb):
     j = names.index("sg_count")
     assert fm.column("sg_m").tolist() == [r[j] for r in case["values"]]
     assert fm.column("sg_count").tolist() == [r[j] for r in tcase["values"]]
+
+
+# ---------------------------------------------------------------- CSV export
+
+def test_csv_export_gpu_matches_host_writer(tmb, tmp_path):
+    """GPU int->text (tm_csv_format) == the host writer, which is
+    byte-identical to engine.py:73-103 (tests/test_host.py)."""
+    import dataclasses
+    from types import SimpleNamespace
+    rng = np.random.default_rng(4)
+    n, e = 700, 40000
+    src = rng.integers(0, n, e)
+    dst = rng.integers(0, n, e)
+    t = rng.integers(0, 5000, e) + 10**9
+    lab = rng.integers(-1, 2, e).astype(np.int8)
+    g = SimpleNamespace(node_count=n, edge_src=src, edge_dst=dst, edge_time=t, edge_label=lab)
+    fm = tmb.mine(g, tmb.full_pattern_set(300))
+    assert fm.device_graph is not None
+    fm.to_csv(str(tmp_path / "gpu.csv"))
+    host = dataclasses.replace(fm, device_graph=None)
+    host.to_csv(str(tmp_path / "host.csv"))
+    assert (tmp_path / "gpu.csv").read_bytes() == (tmp_path / "host.csv").read_bytes()
+    # negative values / unlabeled rows format like "%d" / ""
+    fm2 = dataclasses.replace(fm, values=-fm.values, edge_label=np.full(e, -1, np.int8))
+    fm2.to_csv(str(tmp_path / "gpu2.csv"))
+    dataclasses.replace(fm2, device_graph=None).to_csv(str(tmp_path / "host2.csv"))
+    assert (tmp_path / "gpu2.csv").read_bytes() == (tmp_path / "host2.csv").read_bytes()
