@@ -46,7 +46,10 @@
 namespace tmb {
 namespace {
 
-constexpr int kThreads = 128;        // k_mine_warp block (4 warps)
+#ifndef TM_WARP_THREADS
+#define TM_WARP_THREADS 64  // measured: 64 > 128 > 32 (profiles/)
+#endif
+constexpr int kThreads = TM_WARP_THREADS;  // k_mine_warp block
 constexpr int kWarps = kThreads / 32;
 constexpr int kTaskThreads = 256;
 constexpr int kDomSplit = 256;       // a trigger slice above this becomes domain tasks
@@ -316,7 +319,7 @@ __device__ __forceinline__ void flat_for(WarpShared &ws, int lane, int len, F &&
 }
 
 #ifndef TM_WARP_MINB  // min resident blocks per SM for k_mine_warp (register cap)
-#define TM_WARP_MINB 8  // 64 registers: measured best (profiles/ncu_r01_*)
+#define TM_WARP_MINB 16  // 64 registers at 64 threads: measured best
 #endif
 __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,

@@ -310,3 +310,15 @@ def test_csv_export_gpu_matches_host_writer(tmb, tmp_path):
     fm2.to_csv(str(tmp_path / "gpu2.csv"))
     dataclasses.replace(fm2, device_graph=None).to_csv(str(tmp_path / "host2.csv"))
     assert (tmp_path / "gpu2.csv").read_bytes() == (tmp_path / "host2.csv").read_bytes()
+
+
+def test_members_cfg1(tmb):
+    """cfg1 (alpha = 2.1 giant hub) in members attribution: the reference's
+    generic interpreter needed ~19 min on 8 workers for these 13 columns."""
+    from paper_2604_12241_b200 import synth
+    zm = load_npz("cfg1_members.npz")
+    g0 = synth.generate(synth.CONFIGS["cfg1"])
+    g = tmb.DeviceGraph(g0.src, g0.dst, g0.time)
+    got = tmb.mine_members(g, _mdescs(tmb, columns_of(zm), 86400))
+    g.free()
+    np.testing.assert_array_equal(got, zm["values"])
