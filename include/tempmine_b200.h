@@ -21,6 +21,9 @@
  *   tm_mine_members      the same dispatch with attribution = "members":
  *                        engine.py:629-640 over _EmissionState instances
  *                        engine.py:433-513
+ *   tm_collect_instances mine(..., collect_instances=True) engine.py:629-645,
+ *   tm_fetch_instances   InstanceRecord engine.py:37-52 from _EmissionState
+ *                        engine.py:455-513 (records; host dedup + sort)
  *   tm_csv_format /      FeatureMatrix.to_csv engine.py:73-103 (GPU int->text)
  *   tm_csv_fetch
  *   tm_last_error        Python exceptions EngineInvariantError /
@@ -42,7 +45,7 @@
 extern "C" {
 #endif
 
-#define TM_ABI_VERSION 2
+#define TM_ABI_VERSION 3
 
 /* pattern families (plan.py kernel hints + the extended north-star set) */
 enum tm_family {
@@ -150,6 +153,18 @@ int tm_mine_members(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t
 
 int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats);
 
+/* Instance records of triggers [lo, hi) (engine.py:629-645 with collect):
+ * every instance the reference's _EmissionState appends (engine.py:455-513),
+ * whatever the plan's attribution, as an int32 stream of records
+ *   [plan index, trigger edge, n_edges, n_nodes, edges..., nodes...]
+ * ordered by trigger, then plan.  Edge / node lists may hold duplicates
+ * (the reference's frozensets dedup them) and are unsorted.  The stream
+ * stays on the device; *out_words receives its length in int32 words and
+ * tm_fetch_instances copies the first n_words out (synchronous). */
+int tm_collect_instances(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
+                         int64_t *out_words);
+int tm_fetch_instances(tm_graph *g, int32_t *dst, int64_t n_words);
+
 /* Feature CSV rows (FeatureMatrix.to_csv, engine.py:73-103; header line not
  * included): "edge_id,src,dst,timestamp,label,<features>\n" per edge, "%d"
  * fields, empty label cell when labels is NULL or the label is negative.
@@ -159,6 +174,97 @@ int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats);
 int tm_csv_format(tm_graph *g, const int64_t *values, int values_on_device, int n_cols,
                   const int8_t *labels, int64_t *out_bytes);
 int tm_csv_fetch(tm_graph *g, char *dst, int64_t n_bytes);
+
+/* ---------------------------------------------------------------------
+ * GENERIC stage programs: the reference's generic
+ * interpreter (engine.py:325-562 — execute_cell, _adjacency_map,
+ * _order_satisfiable, run_plan_on_trigger, _EmissionState) as a device VM.
+ * A program is one compiled ExecutionPlan (plan.py:40-91) lowered by the
+ * host: cells in plan order, variables numbered 0 = N0, 1 = N1, 2 + i =
+ * cell i's dst_var; edge symbols 0 = e0, k = eK. */
+#define TM_VM_MAX_CELLS 8
+#define TM_VM_MAX_OPS 4
+#define TM_VM_MAX_PREDS 8
+#define TM_VM_MAX_SYMS 16
+#define TM_VM_TABLE 1024
+
+enum tm_vm_op { TM_VM_FOR_ALL = 0, TM_VM_INTERSECT = 1, TM_VM_UNION = 2, TM_VM_DIFFERENTIATE = 3 };
+enum tm_vm_operand_kind { TM_VM_SCALAR = 0, TM_VM_SET = 1, TM_VM_ADJ = 2, TM_VM_MEMBER_ADJ = 3 };
+enum tm_vm_mode {
+  TM_VM_SET_CARDINALITY = 0, TM_VM_SOURCE_COUNT = 1, TM_VM_PAIR_PRODUCT = 2,
+  TM_VM_EDGE_COUNT = 3, TM_VM_INSTANCE_LIST = 4
+};
+/* comparison operators (engine.py:_compare) */
+enum tm_vm_cmp { TM_VM_EQ = 0, TM_VM_NE = 1, TM_VM_LE = 2, TM_VM_LT = 3, TM_VM_GE = 4, TM_VM_GT = 5 };
+/* value kinds of an edge-predicate term (engine.py:_edge_pred_keeps) */
+enum tm_vm_term {
+  TM_VM_T_NUMBER = 0,   /* num */
+  TM_VM_T_EID = 1,      /* ref 0: the trigger's id, 1: the entry's id */
+  TM_VM_T_TIME = 2,     /* the entry's timestamp */
+  TM_VM_T_AMOUNT = 3,   /* ref 0: trigger, 1: entry */
+  TM_VM_T_CURRENCY = 4, /* ref 0: trigger, 1: entry (compared via vocab rank or table) */
+  TM_VM_T_CONST = 5     /* the whole predicate folds to `num != 0` (type-mismatch ==/!=) */
+};
+
+typedef struct tm_vm_pred {
+  int32_t cmp;          /* enum tm_vm_cmp */
+  int32_t lk, lref;     /* lhs kind (enum tm_vm_term), ref */
+  int32_t rk, rref;
+  int32_t table;        /* currency vs string: offset of a holds[n_vocab] table, else -1 */
+  int32_t sym;          /* edge pred: own symbol it filters; gate pred: bound symbol it tests */
+  int32_t pad;
+  double lnum, rnum;
+} tm_vm_pred;
+
+typedef struct tm_vm_operand {
+  int32_t kind;         /* enum tm_vm_operand_kind */
+  int32_t var;          /* base variable */
+  int32_t slot;         /* referenced cell (set / member_adj), -1 for N0 / N1 */
+  int32_t dir;          /* 0 in_neigh, 1 out_neigh (adjacency kinds) */
+  int32_t sym;          /* edge symbol (adjacency kinds), -1 otherwise */
+} tm_vm_operand;
+
+typedef struct tm_vm_cell {
+  int32_t op;           /* enum tm_vm_op */
+  int32_t parent;       /* -1 at trigger level */
+  int32_t forward;      /* window [t, t + delta] instead of [t - delta, t] */
+  int32_t n_ops;
+  tm_vm_operand ops[TM_VM_MAX_OPS];
+  int32_t n_node, n_edge, n_gate, n_order;
+  int32_t node[TM_VM_MAX_PREDS][3];   /* skip_if var == / != var: cmp, lvar, rvar */
+  tm_vm_pred edge[TM_VM_MAX_PREDS];   /* per-entry skip predicates */
+  tm_vm_pred gate[TM_VM_MAX_PREDS];   /* predicates over already-bound edges */
+  int32_t order[TM_VM_MAX_PREDS][3];  /* cmp, lhs sym, rhs sym (-1 = trigger time t) */
+} tm_vm_cell;
+
+typedef struct tm_vm_program {
+  int32_t n_cells;
+  int32_t mode;         /* enum tm_vm_mode */
+  int32_t min_size;
+  int32_t target[2];    /* emission target cells (pair_product: both) */
+  int32_t uses_attrs;   /* amount / currency terms present: tm_graph_set_attrs first */
+  int64_t delta;
+  tm_vm_cell cells[TM_VM_MAX_CELLS];
+  int8_t table[TM_VM_TABLE];
+} tm_vm_program;
+
+/* Edge attributes for attribute predicates: amount float64[n_edges],
+ * currency int32[n_edges] (vocabulary ids), cur_rank int32[n_vocab] (rank of
+ * each vocabulary string in sorted order).  Host pointers. */
+int tm_graph_set_attrs(tm_graph *g, const double *amount, const int32_t *currency, int32_t n_vocab,
+                       const int32_t *cur_rank);
+
+/* Counts of triggers [lo, hi) into host out[hi - lo] (trigger attribution,
+ * engine.py:607-646 generic branch). */
+int tm_vm_mine(tm_graph *g, const tm_vm_program *prog, int64_t lo, int64_t hi, int64_t *out);
+
+/* Instance records of triggers [lo, hi), tm_collect_instances' format with
+ * `plan_index` in the plan field; fetch with tm_fetch_instances. */
+int tm_vm_collect(tm_graph *g, const tm_vm_program *prog, int32_t plan_index, int64_t lo, int64_t hi,
+                  int64_t *out_words);
+
+/* Members attribution of triggers [lo, hi): host out[n_edges] (overwritten). */
+int tm_vm_members(tm_graph *g, const tm_vm_program *prog, int64_t lo, int64_t hi, int64_t *out);
 
 /* on = 1: bracket the mining kernels of every tm_mine with CUDA events on
  * the launch stream (read back by tm_last_mine_stats). */

@@ -8,18 +8,20 @@ ExecutionPlans or the structurally identical ones `builtin_plan` builds.
 """
 
 from ._lib import TempmineError, UnsupportedPlanError, kernel_launch_count
-from .engine import (EngineInvariantError, FeatureMatrix, last_stats, lower_all, merge_features, mine,
-                     mine_members, mine_rows, mine_rows_device, order_plans)
+from .engine import (EngineInvariantError, FeatureMatrix, InstanceRecord, collect_instance_records,
+                     last_stats, lower_all, merge_features, mine,
+                     mine_members, mine_rows, mine_rows_device, order_plans,
+                     write_instances)
 from .graph import DeviceGraph, GraphStats, as_device_graph
 from .plan import (BUILTIN_COLUMNS, EXTENDED_COLUMNS, FULL_PATTERN_SET, ExecutionPlan, PlanDesc,
                    builtin_plan, canonical_shape, full_pattern_set, load_builtin, lower_plan, recognize)
 
 __all__ = [
     "BUILTIN_COLUMNS", "EXTENDED_COLUMNS", "FULL_PATTERN_SET", "DeviceGraph", "EngineInvariantError",
-    "ExecutionPlan", "FeatureMatrix", "GraphStats", "PlanDesc", "TempmineError",
+    "ExecutionPlan", "FeatureMatrix", "InstanceRecord", "collect_instance_records", "GraphStats", "PlanDesc", "TempmineError",
     "UnsupportedPlanError", "as_device_graph", "builtin_plan", "canonical_shape", "full_pattern_set",
     "kernel_launch_count", "last_stats", "load_builtin", "lower_all", "lower_plan", "merge_features",
-    "mine", "mine_members", "mine_rows", "mine_rows_device", "order_plans", "recognize",
+    "mine", "mine_members", "mine_rows", "mine_rows_device", "order_plans", "recognize", "write_instances",
 ]
 
 __version__ = "0.1.0"

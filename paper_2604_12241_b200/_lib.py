@@ -33,6 +33,36 @@ class TmPlanDesc(ctypes.Structure):
                 ("delta", ctypes.c_int64)]
 
 
+VM_MAX_CELLS, VM_MAX_OPS, VM_MAX_PREDS, VM_MAX_SYMS, VM_TABLE = 8, 4, 8, 16, 1024
+
+
+class TmVmPred(ctypes.Structure):
+    _fields_ = [("cmp", ctypes.c_int32), ("lk", ctypes.c_int32), ("lref", ctypes.c_int32),
+                ("rk", ctypes.c_int32), ("rref", ctypes.c_int32), ("table", ctypes.c_int32),
+                ("sym", ctypes.c_int32), ("pad", ctypes.c_int32), ("lnum", ctypes.c_double),
+                ("rnum", ctypes.c_double)]
+
+
+class TmVmOperand(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("var", ctypes.c_int32), ("slot", ctypes.c_int32),
+                ("dir", ctypes.c_int32), ("sym", ctypes.c_int32)]
+
+
+class TmVmCell(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("parent", ctypes.c_int32), ("forward", ctypes.c_int32),
+                ("n_ops", ctypes.c_int32), ("ops", TmVmOperand * VM_MAX_OPS),
+                ("n_node", ctypes.c_int32), ("n_edge", ctypes.c_int32), ("n_gate", ctypes.c_int32),
+                ("n_order", ctypes.c_int32), ("node", (ctypes.c_int32 * 3) * VM_MAX_PREDS),
+                ("edge", TmVmPred * VM_MAX_PREDS), ("gate", TmVmPred * VM_MAX_PREDS),
+                ("order", (ctypes.c_int32 * 3) * VM_MAX_PREDS)]
+
+
+class TmVmProgram(ctypes.Structure):
+    _fields_ = [("n_cells", ctypes.c_int32), ("mode", ctypes.c_int32), ("min_size", ctypes.c_int32),
+                ("target", ctypes.c_int32 * 2), ("uses_attrs", ctypes.c_int32), ("delta", ctypes.c_int64),
+                ("cells", TmVmCell * VM_MAX_CELLS), ("table", ctypes.c_int8 * VM_TABLE)]
+
+
 class TmGraphInfo(ctypes.Structure):
     _fields_ = [("n_nodes", ctypes.c_int64), ("n_edges", ctypes.c_int64),
                 ("n_ranks", ctypes.c_int64), ("max_out_degree", ctypes.c_int64),
@@ -66,12 +96,20 @@ SIGNATURES = {
     "tm_last_mine_stats": (ctypes.c_int, [_P, ctypes.POINTER(TmMineStats)]),
     "tm_csv_format": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(ctypes.c_int64)]),
     "tm_csv_fetch": (ctypes.c_int, [_P, _P, ctypes.c_int64]),
+    "tm_collect_instances": (ctypes.c_int, [_P, ctypes.POINTER(TmPlanDesc), ctypes.c_int, ctypes.c_int64,
+                                            ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
+    "tm_fetch_instances": (ctypes.c_int, [_P, _P, ctypes.c_int64]),
+    "tm_graph_set_attrs": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, _P]),
+    "tm_vm_mine": (ctypes.c_int, [_P, ctypes.POINTER(TmVmProgram), ctypes.c_int64, ctypes.c_int64, _P]),
+    "tm_vm_collect": (ctypes.c_int, [_P, ctypes.POINTER(TmVmProgram), ctypes.c_int32, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
+    "tm_vm_members": (ctypes.c_int, [_P, ctypes.POINTER(TmVmProgram), ctypes.c_int64, ctypes.c_int64, _P]),
     "tm_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
     "tm_kernel_launch_count": (ctypes.c_int64, []),
     "tm_last_error": (ctypes.c_char_p, []),
     "tm_graph_free": (None, [_P]),
 }
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class TempmineError(RuntimeError):

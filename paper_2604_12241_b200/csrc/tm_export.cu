@@ -152,6 +152,9 @@ int scan64(unsigned long long *a, int64_t n, cudaStream_t s) {
 }
 
 }  // namespace
+
+int scan_u64_exclusive(unsigned long long *a, int64_t n, cudaStream_t s) { return scan64(a, n, s); }
+
 }  // namespace tmb
 
 using namespace tmb;

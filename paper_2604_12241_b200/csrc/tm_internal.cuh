@@ -51,6 +51,12 @@ struct DevGraph {
   const uint32_t *prev[2];
   const int32_t *eid[2];   // edge id per CSR slot (members attribution)
   const int32_t *peid[2];  // edge id per pair slot (members attribution)
+  // window pivots: a slot known to lie inside (or at the edge of) a window,
+  // so window bounds are galloped from it instead of bisecting whole runs
+  const int32_t *eslot[2];  // edge id -> its CSR slot (dir 0: in, 1: out)
+  const int32_t *xpos[2];   // CSR slot -> slot of the same edge in the other CSR
+  const int32_t *tpos[2];   // CSR slot (owner x, nbr n, rank r) -> first slot of
+                            // n's same-direction run with rank >= r
   const uint8_t *loop;
 };
 
@@ -102,6 +108,8 @@ void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);
 int cuda_fail(cudaError_t e, const char *what);
 void count_launch(int n = 1);
+// in-place exclusive scan of n uint64 on stream s (tm_export.cu)
+int scan_u64_exclusive(unsigned long long *a, int64_t n, cudaStream_t s);
 
 #define TM_CUDA(expr)                                       \
   do {                                                      \
@@ -175,11 +183,18 @@ struct tm_graph {
 
   tmb::DevBuf e_src, e_dst, e_rank, uniq_time, loop, maxdeg;
   tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2], peid[2];
+  tmb::DevBuf eslot[2], xpos[2], tpos[2];
 
   // mining scratch (grow-only)
   tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks, split_scratch;
   tmb::DevBuf csv_buf;  // formatted feature CSV (tm_csv_format)
   int64_t csv_bytes = 0;
+  tmb::DevBuf inst_buf;  // instance records (tm_collect_instances, tm_vm_collect)
+  int64_t inst_words = 0;
+  // GENERIC stage programs (tm_vm.cu): edge attributes, program, arena
+  tmb::DevBuf attr_amount, attr_currency, attr_cur_rank;
+  int32_t n_vocab = 0;
+  tmb::DevBuf vm_prog, vm_arena, vm_ovf, vm_novf;
   int64_t lo_tab_cap = 0;
   tm_mine_stats last{};
   bool prof = false, prof_pending = false;

@@ -7,10 +7,12 @@ work runs in libtempmine_b200.so on one GPU; `workers` is accepted for API
 compatibility (the reference's fork-pool width) and has no effect — the
 whole trigger range is one launch, balanced on the device.  Columns with
 attribution "members" go through tm_mine_members (full-matrix
-contributions, engine.py:629-640).  Paths the GPU does not implement
-(instance collection, arbitrary GENERIC stage programs) raise
-UnsupportedPlanError instead of silently falling back to a CPU
-interpreter.
+contributions, engine.py:629-640).  GENERIC plans that match no GPU family
+run on the device stage VM (vm.py, csrc/tm_vm.cu — the reference's generic
+interpreter, engine.py:325-562).  collect_instances=True returns the
+reference's (FeatureMatrix, [InstanceRecord]) pair.  What neither path can
+express raises UnsupportedPlanError instead of silently falling back to a
+CPU interpreter.
 """
 
 from __future__ import annotations
@@ -22,7 +24,8 @@ import numpy as np
 
 from . import _lib
 from .graph import DeviceGraph, as_device_graph
-from .plan import BUILTIN_COLUMNS, PlanDesc, lower_plan
+from .plan import BUILTIN_COLUMNS, GENERIC, PlanDesc, lower_plan
+from .vm import VmProgram, lower_program, vm_instance_stream, vm_members, vm_mine
 
 
 class EngineInvariantError(RuntimeError):
@@ -100,6 +103,25 @@ class FeatureMatrix:
             fh.write(memoryview(buf))
 
 
+@dataclass(frozen=True)
+class InstanceRecord:
+    """One concrete matched instance (member_edges includes the trigger),
+    engine.py:37-52."""
+
+    pattern: str
+    trigger_edge: int
+    member_edges: tuple
+    member_nodes: tuple
+
+    def to_json_dict(self) -> dict:
+        return {
+            "pattern": self.pattern,
+            "trigger_edge": self.trigger_edge,
+            "member_edges": list(self.member_edges),
+            "member_nodes": list(self.member_nodes),
+        }
+
+
 def merge_features(partials: list) -> FeatureMatrix:
     """engine.py:106-120 — elementwise integer sum."""
     if not partials:
@@ -127,15 +149,26 @@ def order_plans(plans: list) -> list:
     return builtin + custom
 
 
-def lower_all(plans: list) -> tuple[list, list[PlanDesc]]:
+def lower_all(plans: list, vocab=None, allow_vm: bool = False) -> tuple[list, list]:
+    """Ordered plans and their lowering: a PlanDesc per family plan and, with
+    allow_vm, a VmProgram per GENERIC plan no family matches."""
     plans = order_plans(list(plans))
     for p in plans:
         if p.slot_count != len(p.cells):
             raise EngineInvariantError(f"plan {p.name}: slot count disagrees with cells")
-    descs = [lower_plan(p) for p in plans]
-    if len(descs) > _lib.MAX_PLANS:
-        raise ValueError(f"at most {_lib.MAX_PLANS} columns per mine() call")
-    return plans, descs
+    items = []
+    for p in plans:
+        try:
+            items.append(lower_plan(p))
+        except _lib.UnsupportedPlanError:
+            if not allow_vm or getattr(p, "kernel_hint", GENERIC) != GENERIC:
+                raise
+            items.append(lower_program(p, vocab))
+    return plans, items
+
+
+def _chunks(idx: list, n: int = _lib.MAX_PLANS):
+    return [idx[i:i + n] for i in range(0, len(idx), n)]
 
 
 def mine_members(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int = 0, hi: int | None = None,
@@ -182,6 +215,56 @@ def mine_rows_device(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: in
     _lib.check(rc, "tm_mine")
 
 
+# triggers per tm_collect_instances call: bounds the device record stream
+INSTANCE_CHUNK = 1 << 16
+
+
+def instance_stream(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int) -> np.ndarray:
+    """Raw int32 record stream of triggers [lo, hi) (tempmine_b200.h:
+    [plan, trigger, n_edges, n_nodes, edges..., nodes...] per record)."""
+    if hi <= lo or not descs:
+        return np.zeros(0, dtype=np.int32)
+    lib = _lib.load()
+    arr = _lib.plan_array(descs)
+    words = ctypes.c_int64()
+    _lib.check(lib.tm_collect_instances(dgraph.handle, arr, len(descs), lo, hi, ctypes.byref(words)),
+               "tm_collect_instances")
+    buf = np.empty(words.value, dtype=np.int32)
+    _lib.check(lib.tm_fetch_instances(dgraph.handle, _lib.ptr(buf), words.value), "tm_fetch_instances")
+    return buf
+
+
+def decode_instances(buf: np.ndarray, names: list) -> list:
+    """Records -> InstanceRecord with member sets deduplicated and sorted
+    (tuple(sorted(frozenset)), engine.py:641-645)."""
+    out = []
+    n = len(buf)
+    p = 0
+    data = buf.tolist()
+    while p < n:
+        ci, trig, ne, nn = data[p], data[p + 1], data[p + 2], data[p + 3]
+        q = p + 4 + ne
+        out.append(InstanceRecord(names[ci], trig, tuple(sorted(set(data[p + 4:q]))),
+                                  tuple(sorted(set(data[q:q + nn])))))
+        p = q + nn
+    if p != n:
+        raise EngineInvariantError("truncated instance stream")
+    return out
+
+
+def collect_instance_records(dgraph: DeviceGraph, descs: list[PlanDesc], names: list, lo: int = 0,
+                             hi: int | None = None, sort: bool = True) -> list:
+    """Every instance found at triggers [lo, hi), sorted like mine()'s
+    (pattern, trigger_edge, member_edges) (engine.py:710-711)."""
+    hi = dgraph.edge_count if hi is None else hi
+    recs = []
+    for a in range(lo, hi, INSTANCE_CHUNK):
+        recs += decode_instances(instance_stream(dgraph, descs, a, min(a + INSTANCE_CHUNK, hi)), names)
+    if sort:
+        recs.sort(key=lambda r: (r.pattern, r.trigger_edge, r.member_edges))
+    return recs
+
+
 def last_stats(dgraph: DeviceGraph) -> _lib.TmMineStats:
     st = _lib.TmMineStats()
     _lib.check(_lib.load().tm_last_mine_stats(dgraph.handle, ctypes.byref(st)), "tm_last_mine_stats")
@@ -197,24 +280,44 @@ def mine(graph, plans, workers: int = 1, collect_instances: bool = False, *, dev
     """
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
-    if collect_instances:  # instance records are a separate §8f row
-        raise _lib.UnsupportedPlanError(
-            _lib.TM_E_UNSUPPORTED_PLAN,
-            "collect_instances=True needs per-instance records, which the GPU path does not emit")
-    plans, descs = lower_all(plans)
+    vocab = getattr(graph, "currency_vocab", None)
+    plans, items = lower_all(plans, vocab, allow_vm=True)
     dg = as_device_graph(graph, device)
-    trig = [i for i, d in enumerate(descs) if not d.members]
-    memb = [i for i, d in enumerate(descs) if d.members]
-    if not memb:
-        values = mine_rows(dg, descs, 0, dg.edge_count)
-    else:
-        values = np.empty((dg.edge_count, len(descs)), dtype=np.int64)
-        if trig:
-            values[:, trig] = mine_rows(dg, [descs[i] for i in trig], 0, dg.edge_count)
-        values[:, memb] = mine_members(dg, [descs[i] for i in memb])
+    E = dg.edge_count
+    values = np.zeros((E, len(items)), dtype=np.int64)
+    trig = [i for i, d in enumerate(items) if isinstance(d, PlanDesc) and not d.members]
+    memb = [i for i, d in enumerate(items) if isinstance(d, PlanDesc) and d.members]
+    for part in _chunks(trig):
+        values[:, part] = mine_rows(dg, [items[i] for i in part], 0, E)
+    for part in _chunks(memb):
+        values[:, part] = mine_members(dg, [items[i] for i in part])
+    for i, d in enumerate(items):
+        if isinstance(d, VmProgram):
+            values[:, i] = vm_members(dg, d) if d.members else vm_mine(dg, d)
     label = getattr(graph, "edge_label", None)
     if label is None:
         label = dg.edge_label
-    return FeatureMatrix(columns=tuple(p.name for p in plans), values=values,
-                         edge_src=graph.edge_src, edge_dst=graph.edge_dst,
-                         edge_time=graph.edge_time, edge_label=label, device_graph=dg)
+    fm = FeatureMatrix(columns=tuple(p.name for p in plans), values=values,
+                       edge_src=graph.edge_src, edge_dst=graph.edge_dst,
+                       edge_time=graph.edge_time, edge_label=label, device_graph=dg)
+    if not collect_instances:
+        return fm
+    names = [p.name for p in plans]
+    fam = [i for i, d in enumerate(items) if isinstance(d, PlanDesc)]
+    recs = []
+    for part in _chunks(fam):
+        recs += collect_instance_records(dg, [items[i] for i in part], [names[i] for i in part], sort=False)
+    for i, d in enumerate(items):
+        if isinstance(d, VmProgram):
+            for a in range(0, E, INSTANCE_CHUNK):
+                recs += decode_instances(vm_instance_stream(dg, d, 0, a, min(a + INSTANCE_CHUNK, E)), [names[i]])
+    recs.sort(key=lambda r: (r.pattern, r.trigger_edge, r.member_edges))
+    return fm, recs
+
+
+def write_instances(path: str, instances: list) -> None:
+    """JSONL as the reference CLI writes it (cli.py:163-167)."""
+    import json
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        for inst in instances:
+            fh.write(json.dumps(inst.to_json_dict(), separators=(",", ":")) + "\n")

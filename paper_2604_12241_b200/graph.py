@@ -44,7 +44,8 @@ class DeviceGraph:
     """
 
     def __init__(self, edge_src, edge_dst, edge_time, node_count: int | None = None,
-                 edge_label=None, device: int = 0, stream: int | None = None):
+                 edge_label=None, device: int = 0, stream: int | None = None, edge_amount=None,
+                 edge_currency=None, currency_vocab=None):
         lib = _lib.load()
         src = _as_i64(edge_src, "edge_src")
         dst = _as_i64(edge_dst, "edge_dst")
@@ -68,11 +69,38 @@ class DeviceGraph:
         self._finalizer = weakref.finalize(self, lib.tm_graph_free, handle)
         self._stats: GraphStats | None = None
         self._csr: dict = {}
+        # edge attributes (txgraph.py:113-123), uploaded on first use by an
+        # attribute predicate of a GENERIC stage program
+        self.edge_amount = edge_amount
+        self.edge_currency = edge_currency
+        self.currency_vocab = tuple(currency_vocab) if currency_vocab is not None else None
+        self._attrs_on_device = False
+
+    def ensure_attrs(self) -> None:
+        """Upload amount / currency / vocabulary ranks (tm_graph_set_attrs)."""
+        if self._attrs_on_device:
+            return
+        if self.edge_amount is None or self.edge_currency is None or self.currency_vocab is None:
+            raise ValueError("attribute predicates need edge_amount, edge_currency and currency_vocab")
+        amount = np.ascontiguousarray(self.edge_amount, dtype=np.float64)
+        cur = np.ascontiguousarray(self.edge_currency, dtype=np.int32)
+        if len(amount) != self.edge_count or len(cur) != self.edge_count:
+            raise ValueError("attribute arrays differ in length from the edge table")
+        vocab = self.currency_vocab
+        order = sorted(range(len(vocab)), key=lambda i: vocab[i])
+        rank = np.empty(len(vocab), dtype=np.int32)
+        rank[order] = np.arange(len(vocab), dtype=np.int32)
+        _lib.check(_lib.load().tm_graph_set_attrs(self.handle, _lib.ptr(amount), _lib.ptr(cur), len(vocab),
+                                                  _lib.ptr(rank)), "tm_graph_set_attrs")
+        self._attrs_on_device = True
 
     @classmethod
     def from_graph(cls, graph, device: int = 0) -> "DeviceGraph":
         return cls(graph.edge_src, graph.edge_dst, graph.edge_time, node_count=graph.node_count,
-                   edge_label=getattr(graph, "edge_label", None), device=device)
+                   edge_label=getattr(graph, "edge_label", None), device=device,
+                   edge_amount=getattr(graph, "edge_amount", None),
+                   edge_currency=getattr(graph, "edge_currency", None),
+                   currency_vocab=getattr(graph, "currency_vocab", None))
 
     @property
     def handle(self) -> ctypes.c_void_p:

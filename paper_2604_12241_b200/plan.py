@@ -243,6 +243,22 @@ def builtin_plan(name: str, delta: int | None = None, min_size: int | None = Non
     return b.plan(column or name, delta, mode, targets, k, hint if hinted else GENERIC)
 
 
+def plan_from_dict(d: dict) -> ExecutionPlan:
+    """Rebuild a compiled plan from dataclasses.asdict() of a reference (or
+    our) ExecutionPlan — how compiled custom patterns travel as fixtures."""
+    t = lambda x: Term(x["kind"], x["name"], x["attr"], x["value"])  # noqa: E731
+    c = lambda x: ConstraintExpr(x["kind"], t(x["lhs"]), x["op"], t(x["rhs"]))  # noqa: E731
+    cells = tuple(LoopCell(cl["op"], tuple(OperandDesc(**o) for o in cl["src"]), cl["dst_slot"],
+                           cl["dst_var"], cl["parent"], tuple(c(p) for p in cl["skip_preds"]),
+                           tuple(c(p) for p in cl["order_preds"]), cl["window_lo"], cl["window_hi"])
+                  for cl in d["cells"])
+    em = d["emission"]
+    return ExecutionPlan(d["name"], d["delta"], cells, d["slot_count"],
+                         CompiledEmission(em["mode"], em["min_size"], tuple(em["target_slots"]),
+                                          tuple(em["target_vars"])), d["kernel_hint"],
+                         d.get("attribution", "trigger"))
+
+
 def load_builtin(name: str, delta: int | None = None, min_size: int | None = None) -> ExecutionPlan:
     if name not in BUILTIN_COLUMNS:
         raise KeyError(f"no builtin pattern {name!r}")

@@ -438,6 +438,393 @@ def make_plans():
     print(f"plans.json: {len(entries)} plans")
 
 
+# ---------------------------------------------------------------------------
+# instance lists (mine(..., collect_instances=True), engine.py:629-645,
+# 658-720): every instance _EmissionState records (engine.py:455-513) as
+# InstanceRecord(pattern, trigger_edge, sorted member_edges, sorted
+# member_nodes), sorted by (pattern, trigger_edge, member_edges).  Stored as
+# one int32 stream per case: [pattern index, trigger, n_edges, n_nodes,
+# edges..., nodes...] per record, in the reference's order.
+
+INSTANCE_CORPUS = 24      # first graphs of the acceptance corpus, smallest delta
+
+
+def collect_records(g: TemporalGraph, specs, delta: int, workers: int = 1) -> np.ndarray:
+    pats = patterns_for(specs, delta)
+    plans = [compile_pattern(p, g.stats) for p in pats]
+    _, inst = mine(g, plans, workers=workers, collect_instances=True)
+    col = {c: i for i, (c, _, _) in enumerate(specs)}
+    out = []
+    for r in inst:
+        out += [col[r.pattern], r.trigger_edge, len(r.member_edges), len(r.member_nodes)]
+        out += list(r.member_edges) + list(r.member_nodes)
+    return np.array(out, dtype=np.int32)
+
+
+def _corpus_one_instances(p):
+    seed, n_nodes, n_edges, horizon, deltas = p
+    edges = corpus_records(seed, n_nodes, n_edges, horizon)
+    g = graph_from_edges(edges)
+    return collect_records(g, CORPUS_SPECS, int(deltas[0]))
+
+
+def make_instances():
+    arrays, meta = {}, []
+    for name, (edges, deltas) in HAND_GRAPHS.items():
+        g = graph_from_edges(edges)
+        for delta in deltas:
+            arrays[f"rec{len(meta)}"] = collect_records(g, ALL_SPECS, delta)
+            arrays[f"edges{len(meta)}"] = np.array(edges, dtype=np.int64).reshape(-1, 3)
+            meta.append({"name": name, "delta": delta, "specs": "all"})
+    params = corpus_params()[:INSTANCE_CORPUS]
+    with multiprocessing.get_context("fork").Pool(os.cpu_count()) as pool:
+        res = pool.map(_corpus_one_instances, params, chunksize=1)
+    for i, (p, rec) in enumerate(zip(params, res)):
+        seed, n_nodes, n_edges, horizon, deltas = p
+        arrays[f"rec{len(meta)}"] = rec
+        arrays[f"edges{len(meta)}"] = np.array(corpus_records(seed, n_nodes, n_edges, horizon),
+                                               dtype=np.int64)
+        meta.append({"name": f"corpus{i}", "delta": int(deltas[0]), "specs": "corpus"})
+    z = np.load(OUT / "ties.npz")  # self-loops + same-tick ties, delta 0
+    src, dst, t = (z[f"{k}0"].astype(np.int64) for k in ("src", "dst", "time"))
+    arrays[f"rec{len(meta)}"] = collect_records(graph_from_arrays(src, dst, t), ALL_SPECS, 0,
+                                                workers=os.cpu_count())
+    arrays[f"edges{len(meta)}"] = np.stack([src, dst, t], axis=1)
+    meta.append({"name": "ties0", "delta": 0, "specs": "all"})
+    n = sum(len(a) for k, a in arrays.items() if k.startswith("rec"))
+    np.savez_compressed(OUT / "instances.npz", meta=json.dumps(meta),
+                        all_columns=json.dumps(spec_json(ALL_SPECS)),
+                        corpus_columns=json.dumps(spec_json(CORPUS_SPECS)), **arrays)
+    print(f"instances.npz: {len(meta)} cases, {n} record words")
+
+
+# ---------------------------------------------------------------------------
+# GENERIC stage programs: the reference's shipped custom
+# patterns (tests/data/custom/*.pat) plus programs written here from the
+# grammar (pattern_grammar.md) to reach every interpreter feature: union /
+# differentiate, set references (bound X.self, siblings), 3-deep nests,
+# forward windows, order constraints (with t), edge-identity, amount and
+# currency predicates, gates on e0 and on an enclosing symbol, every
+# emission mode, min_size > 1.  Expected values: tempmine.engine.mine on
+# compile_pattern(force_generic=True) plans.
+
+VM_PATTERNS = {
+    "union3": """pattern: union3
+delta: {delta}
+stage:
+  op: union
+  src: N0.out_neigh, N1.out_neigh, N1.in_neigh
+  dst_var: U
+  skip_if: U == N0
+emit:
+  mode: set_cardinality
+  target: U
+""",
+    "fwd_fan": """pattern: fwd_fan
+delta: {delta}
+stage:
+  op: for_all
+  src: N1.out_neigh
+  dst_var: F
+  window: forward
+  skip_if: e1 == e0
+  break_if: e1.t > t + delta
+emit:
+  mode: edge_count
+  min_size: 2
+  target: F
+""",
+    "ord_cycle3": """pattern: ord_cycle3
+delta: {delta}
+stage:
+  op: for_all
+  src: N1.out_neigh
+  dst_var: A
+  skip_if: A == N0
+stage:
+  op: intersect
+  src: A.out_neigh, N0.in_neigh
+  dst_var: C
+  skip_if: C == N1
+  order: e1.t <= e2.t
+  order: e2.t <= e3.t
+  order: e3.t <= t
+emit:
+  mode: set_cardinality
+  target: C
+""",
+    "big_out": """pattern: big_out
+delta: {delta}
+stage:
+  op: for_all
+  src: N0.out_neigh
+  dst_var: X
+  skip_if: e1.amount < 500
+  skip_if: e1 == e0
+emit:
+  mode: instance_list
+  target: X
+""",
+    "gate_cur": """pattern: gate_cur
+delta: {delta}
+stage:
+  op: for_all
+  src: N1.in_neigh
+  dst_var: S
+  skip_if: e0.amount > 700
+  skip_if: e1.currency != "USD"
+emit:
+  mode: set_cardinality
+  target: S
+""",
+    "same_cur_stack": """pattern: same_cur_stack
+delta: {delta}
+stage:
+  op: for_all
+  src: N0.in_neigh
+  dst_var: A
+  skip_if: e1.currency != e0.currency
+  skip_if: A == N1
+stage:
+  op: for_all
+  src: N1.out_neigh
+  dst_var: C
+  window: forward
+  skip_if: e2.currency > e0.currency
+  skip_if: C == N0
+emit:
+  mode: pair_product
+  target: A, C
+""",
+    "nest_self": """pattern: nest_self
+delta: {delta}
+stage:
+  op: for_all
+  src: N1.out_neigh
+  dst_var: A
+  skip_if: A == N0
+stage:
+  op: for_all
+  src: A.out_neigh
+  dst_var: B
+  skip_if: B == N1
+  skip_if: B == N0
+stage:
+  op: intersect
+  src: B.out_neigh, A.self
+  dst_var: C
+stage:
+  op: differentiate
+  src: C.self
+  dst_var: D
+  skip_if: D == N1
+emit:
+  mode: source_count
+  target: D
+""",
+    "gate_anc": """pattern: gate_anc
+delta: {delta}
+stage:
+  op: for_all
+  src: N0.in_neigh
+  dst_var: S
+  skip_if: S == N1
+stage:
+  op: intersect
+  src: S.out_neigh, N1.in_neigh
+  dst_var: M
+  skip_if: e1.amount > 300
+emit:
+  mode: source_count
+  target: M
+""",
+    "union_sets": """pattern: union_sets
+delta: {delta}
+stage:
+  op: for_all
+  src: N0.in_neigh
+  dst_var: A
+stage:
+  op: for_all
+  src: N1.out_neigh
+  dst_var: B
+stage:
+  op: union
+  src: A.self, B.self
+  dst_var: U
+  skip_if: U == N0
+  skip_if: U == N1
+emit:
+  mode: set_cardinality
+  min_size: 2
+  target: U
+""",
+    "set_adj": """pattern: set_adj
+delta: {delta}
+stage:
+  op: for_all
+  src: N0.in_neigh
+  dst_var: A
+stage:
+  op: intersect
+  src: A.self, N1.out_neigh
+  dst_var: X
+emit:
+  mode: set_cardinality
+  target: X
+""",
+    "sibling_ref": """pattern: sibling_ref
+delta: {delta}
+stage:
+  op: for_all
+  src: N0.in_neigh
+  dst_var: P
+stage:
+  op: for_all
+  src: N1.out_neigh
+  dst_var: A
+  skip_if: A == N0
+stage:
+  op: intersect
+  src: A.out_neigh, P.self
+  dst_var: Q
+  order: e3.t < e2.t
+emit:
+  mode: set_cardinality
+  target: Q
+""",
+    "fwd_order": """pattern: fwd_order
+delta: {delta}
+stage:
+  op: for_all
+  src: N1.out_neigh
+  dst_var: A
+  window: forward
+  skip_if: A == N0
+stage:
+  op: intersect
+  src: A.out_neigh, N0.in_neigh
+  dst_var: C
+  window: forward
+  order: e2.t >= e1.t
+  order: e3.t > t
+emit:
+  mode: source_count
+  min_size: 1
+  target: C
+""",
+    "amt_edges": """pattern: amt_edges
+delta: {delta}
+stage:
+  op: for_all
+  src: N0.in_neigh
+  dst_var: I
+  skip_if: e1.amount >= 250.5
+  skip_if: e1.currency == "EUR"
+stage:
+  op: for_all
+  src: I.in_neigh
+  dst_var: J
+  skip_if: J == N0
+  skip_if: e2.amount < e1.amount
+emit:
+  mode: edge_count
+  min_size: 2
+  target: J
+""",
+}
+VM_CUSTOMS = ("spray_union", "filtered_senders", "sg_ordered", "stack_forward", "chain_5cycle")
+VM_VOCAB = ("USD", "EUR", "GBP", "CHF")
+
+
+def vm_texts(delta: int, attribution: str = "trigger") -> dict:
+    import re
+    out = {}
+    for name in VM_CUSTOMS:
+        txt = (CUSTOM_DIR / f"{name}.pat").read_text()
+        out[name] = re.sub(r"(?m)^delta:.*$", f"delta: {delta}", txt)
+    for name, tmpl in VM_PATTERNS.items():
+        out[name] = tmpl.replace("{delta}", str(delta))
+    if attribution != "trigger":
+        out = {n: re.sub(r"(?m)^(delta:.*)$", rf"\1\nattribution: {attribution}", t) for n, t in out.items()}
+    return out
+
+
+def vm_plans(delta: int, attribution: str = "trigger"):
+    return [compile_pattern(dsl.must_validate(dsl.parse_pattern(t)), None, force_generic=True)
+            for t in vm_texts(delta, attribution).values()]
+
+
+def vm_graph(edges):
+    """edges (src, dst, t) with deterministic amounts / currencies."""
+    recs = [TransactionRecord(i, int(e[0]), int(e[1]), int(e[2]), float(50 + (i * 37) % 1000),
+                              VM_VOCAB[(i * 3 + i // 5) % 4]) for i, e in enumerate(edges)]
+    return build_graph(recs)
+
+
+def vm_case(edges, delta, want_instances):
+    g = vm_graph(edges)
+    plans = vm_plans(delta)
+    fm = mine(g, plans)
+    counts = np.stack([fm.column(p.name) for p in plans], axis=1)
+    fmm = mine(g, vm_plans(delta, "members"))
+    members = np.stack([fmm.column(p.name) for p in plans], axis=1)
+    rec = np.zeros(0, dtype=np.int32)
+    if want_instances:
+        _, inst = mine(g, plans, collect_instances=True)
+        col = {p.name: i for i, p in enumerate(plans)}
+        out = []
+        for r in inst:
+            out += [col[r.pattern], r.trigger_edge, len(r.member_edges), len(r.member_nodes)]
+            out += list(r.member_edges) + list(r.member_nodes)
+        rec = np.array(out, dtype=np.int32)
+    return (np.asarray(edges, dtype=np.int64).reshape(-1, 3), g.edge_amount.copy(),
+            g.edge_currency.copy(), tuple(g.currency_vocab), counts, members, rec)
+
+
+def _vm_one(args):
+    return vm_case(*args)
+
+
+VM_CORPUS = 40
+
+
+def make_vm():
+    vm_plans(0), vm_plans(5, "members")  # validate every program up front
+    jobs, meta = [], []
+    for name, (edges, deltas) in HAND_GRAPHS.items():
+        for d in deltas:
+            jobs.append((edges, d, True))
+            meta.append({"name": name, "delta": d})
+    for i, p in enumerate(corpus_params()[:VM_CORPUS]):
+        seed, n_nodes, n_edges, horizon, deltas = p
+        edges = corpus_records(seed, n_nodes, n_edges, horizon)
+        for k, d in enumerate(deltas):
+            jobs.append((edges, int(d), k == 0 and i < 24))
+            meta.append({"name": f"corpus{i}", "delta": int(d)})
+    z = np.load(OUT / "ties.npz")
+    te = np.stack([z["src0"], z["dst0"], z["time0"]], axis=1).astype(np.int64)
+    for d in (0, 2):
+        jobs.append((te.tolist(), d, False))
+        meta.append({"name": "ties0", "delta": d})
+    t0 = time.time()
+    with multiprocessing.get_context("fork").Pool(os.cpu_count()) as pool:
+        res = pool.map(_vm_one, jobs, chunksize=1)
+    arrays = {}
+    for k, (edges, amount, cur, vocab, counts, members, rec) in enumerate(res):
+        meta[k]["vocab"] = list(vocab)
+        arrays[f"edges{k}"] = edges
+        arrays[f"amount{k}"] = amount
+        arrays[f"currency{k}"] = cur
+        arrays[f"counts{k}"] = counts
+        arrays[f"members{k}"] = members
+        arrays[f"rec{k}"] = rec
+    plans = [dataclasses.asdict(p) for p in vm_plans(0)]
+    np.savez_compressed(OUT / "vm.npz", meta=json.dumps(meta), plans=json.dumps(plans), **arrays)
+    words = sum(len(r[-1]) for r in res)
+    print(f"vm.npz: {len(meta)} cases, {len(plans)} programs, {words} record words, {time.time() - t0:.0f}s")
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["hand", "corpus", "ties", "cfg1"]
     for w in which:

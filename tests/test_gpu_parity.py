@@ -201,8 +201,12 @@ def test_mine_api_drop_in(tmb):
         tmb.mine(g, plans, workers=0)
     with pytest.raises(tmb.EngineInvariantError):
         tmb.mine(g, plans + [tmb.builtin_plan("fan_in", 3)])
-    with pytest.raises(tmb.UnsupportedPlanError):
-        tmb.mine(g, plans, collect_instances=True)
+    fm2, inst = tmb.mine(g, plans, collect_instances=True)
+    np.testing.assert_array_equal(fm2.values, fm.values)
+    sg = [r for r in inst if r.pattern == "sg_count"]
+    # as the reference prints them (tempmine.engine.mine, collect_instances=True)
+    assert [(r.trigger_edge, r.member_edges, r.member_nodes) for r in sg] == [
+        (4, (0, 1, 3, 4), (0, 1, 2, 3)), (5, (0, 1, 2, 3, 4, 5), (0, 1, 2, 3, 4))]
 
 
 def test_bad_graphs_raise(tmb):
@@ -322,3 +326,57 @@ def test_members_cfg1(tmb):
     got = tmb.mine_members(g, _mdescs(tmb, columns_of(zm), 86400))
     g.free()
     np.testing.assert_array_equal(got, zm["values"])
+
+
+def test_empty_and_tiny_graphs(tmb):
+    """E = 0 and E = 1: shapes and values as the reference (mine over no
+    triggers returns an (E, C) int64 block)."""
+    from types import SimpleNamespace
+    e0 = np.zeros(0, dtype=np.int64)
+    g = SimpleNamespace(node_count=0, edge_src=e0, edge_dst=e0, edge_time=e0,
+                        edge_label=np.zeros(0, np.int8))
+    fm = tmb.mine(g, tmb.full_pattern_set(100))
+    assert fm.values.shape == (0, 14) and fm.values.dtype == np.int64
+    import dataclasses
+    m = dataclasses.replace(tmb.builtin_plan("stack_count", 5), name="st_m", attribution="members")
+    assert tmb.mine(g, [m]).values.shape == (0, 1)
+    one = SimpleNamespace(node_count=2, edge_src=np.array([0]), edge_dst=np.array([1]),
+                          edge_time=np.array([5]), edge_label=np.array([-1], np.int8))
+    fm1 = tmb.mine(one, tmb.full_pattern_set(0) + [m])
+    assert fm1.column("deg_out_src").tolist() == [1] and fm1.column("deg_in_dst").tolist() == [1]
+    assert int(fm1.values.sum()) == 2
+
+
+# ---------------------------------------------------------------- instance lists
+
+def _encode(recs, col_index):
+    out = []
+    for r in recs:
+        out += [col_index[r.pattern], r.trigger_edge, len(r.member_edges), len(r.member_nodes)]
+        out += list(r.member_edges) + list(r.member_nodes)
+    return np.array(out, dtype=np.int64)
+
+
+def test_instances_vs_reference(tmb):
+    """collect_instances records (engine.py:629-645, 710-711) against the
+    reference's own InstanceRecord lists: hand graphs at every delta and the
+    first acceptance-corpus graphs (tests/golden/instances.npz)."""
+    from paper_2604_12241_b200.engine import collect_instance_records
+    z = load_npz("instances.npz")
+    meta = json.loads(str(z["meta"]))
+    cols_by = {"all": json.loads(str(z["all_columns"])), "corpus": json.loads(str(z["corpus_columns"]))}
+    total = 0
+    for k, m in enumerate(meta):
+        cols = cols_by[m["specs"]]
+        e = z[f"edges{k}"].astype(np.int64)
+        g = tmb.DeviceGraph(e[:, 0], e[:, 1], e[:, 2])
+        recs = []
+        for part in _split(tmb, cols):
+            recs += collect_instance_records(g, _descs(tmb, part, m["delta"]), [c["column"] for c in part])
+        g.free()
+        recs.sort(key=lambda r: (r.pattern, r.trigger_edge, r.member_edges))
+        got = _encode(recs, {c["column"]: i for i, c in enumerate(cols)})
+        want = z[f"rec{k}"].astype(np.int64)
+        assert got.shape == want.shape and np.array_equal(got, want), f"{m['name']} d={m['delta']}"
+        total += len(recs)
+    assert total > 1000

@@ -108,3 +108,23 @@ def test_merge_features():
     assert merge_features([a, b]).values.tolist() == [[4, 6]]
     with pytest.raises(EngineInvariantError):
         merge_features([])
+
+
+def test_instance_stream_decode_and_jsonl(tmp_path):
+    """Host half of collect_instances: records -> InstanceRecord with member
+    sets deduped + sorted (engine.py:641-645) and the CLI JSONL (cli.py:163-167)."""
+    import json
+    from paper_2604_12241_b200.engine import InstanceRecord, decode_instances, write_instances
+    buf = np.array([1, 7, 4, 3, 7, 2, 7, 5, 9, 3, 9,
+                    0, 2, 1, 2, 2, 0, 1], dtype=np.int32)
+    recs = decode_instances(buf, ["fan_in", "sg_count"])
+    assert recs == [InstanceRecord("sg_count", 7, (2, 5, 7), (3, 9)),
+                    InstanceRecord("fan_in", 2, (2,), (0, 1))]
+    with pytest.raises(Exception):
+        decode_instances(buf[:-1], ["fan_in", "sg_count"])
+    path = tmp_path / "inst.jsonl"
+    write_instances(str(path), recs)
+    lines = path.read_text().splitlines()
+    assert json.loads(lines[0]) == {"pattern": "sg_count", "trigger_edge": 7,
+                                    "member_edges": [2, 5, 7], "member_nodes": [3, 9]}
+    assert lines[1] == '{"pattern":"fan_in","trigger_edge":2,"member_edges":[2],"member_nodes":[0,1]}'

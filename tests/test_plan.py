@@ -29,16 +29,7 @@ EXPECTED = {
 
 def _obj(d):
     """Rebuild a reference ExecutionPlan (from dataclasses.asdict) as objects."""
-    t = lambda x: P.Term(x["kind"], x["name"], x["attr"], x["value"])
-    c = lambda x: P.ConstraintExpr(x["kind"], t(x["lhs"]), x["op"], t(x["rhs"]))
-    cells = tuple(P.LoopCell(cl["op"], tuple(P.OperandDesc(**o) for o in cl["src"]), cl["dst_slot"],
-                             cl["dst_var"], cl["parent"], tuple(c(p) for p in cl["skip_preds"]),
-                             tuple(c(p) for p in cl["order_preds"]), cl["window_lo"], cl["window_hi"])
-                  for cl in d["cells"])
-    em = d["emission"]
-    return P.ExecutionPlan(d["name"], d["delta"], cells, d["slot_count"],
-                           P.CompiledEmission(em["mode"], em["min_size"], tuple(em["target_slots"]),
-                                              tuple(em["target_vars"])), d["kernel_hint"], d["attribution"])
+    return P.plan_from_dict(d)
 
 
 def _entries():

@@ -1,0 +1,46 @@
+"""BASELINE configs[4]: cycle length (2..8) x window (1 h .. 7 d) on the
+HI-Medium shape, 1 B200.  One column per run (cycle_L alone), device-resident
+graph; prints one JSON line per (L, delta) with ms and edges/s.
+
+    python tools/sweep_cycles.py [hi-medium] [--deltas 3600,21600,86400,259200,604800]
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2604_12241_b200 as tmb  # noqa: E402
+from paper_2604_12241_b200 import _lib, synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("config", nargs="?", default="hi-medium")
+ap.add_argument("--deltas", default="3600,21600,86400,259200,604800")
+ap.add_argument("--lengths", default="2,3,4,5,6,7,8")
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+
+g0 = synth.time_ordered(synth.generate(synth.CONFIGS[a.config]))
+g = tmb.DeviceGraph(g0.src, g0.dst, g0.time, node_count=g0.node_count)
+_lib.check(_lib.load().tm_set_profiling(g.handle, 1), "prof")
+E = g.edge_count
+stream = torch.cuda.Stream()
+out = torch.empty((E, 1), dtype=torch.int64, device="cuda")
+for L in [int(x) for x in a.lengths.split(",")]:
+    for d in [int(x) for x in a.deltas.split(",")]:
+        descs = [tmb.lower_plan(tmb.builtin_plan(f"cycle_{L}", d))]
+        best = None
+        for rep in range(a.reps + 1):
+            tmb.mine_rows_device(g, descs, 0, E, out.data_ptr(), stream.cuda_stream)
+            st = tmb.last_stats(g)
+            if rep and (best is None or st.total_ms < best.total_ms):
+                best = st
+        total = int(out.sum().item())
+        print(json.dumps({"config": a.config, "cycle_len": L, "delta": d, "ms": best.total_ms,
+                          "warp_ms": best.light_ms, "task_ms": best.heavy_ms,
+                          "edges_per_s": E / (best.total_ms / 1e3), "column_sum": total}), flush=True)
