@@ -112,87 +112,6 @@ __device__ __forceinline__ void fill_windows(Ctx &c, int need) {
 #endif
 }
 
-// ------------------------------------------------------------ pivoted windows
-//
-// A pivot p of x's dir-run is a slot with lb(lo) <= p <= ub(hi), i.e. the
-// window's lower bound is at or before p and its upper bound at or after p.
-// Exact pivots (the slot of an edge known to be inside the window) and
-// time-aligned pivots (first slot at rank >= r for some r in [lo, hi]) both
-// qualify.  The two bounds are galloped outward from p independently (their
-// loads overlap); kGallop probes, then a bisection of what is left, so a
-// wide window costs at most kGallop loads more than a plain bisection.
-#ifndef TM_PIVOT
-#define TM_PIVOT 1
-#endif
-constexpr int kGallop = 4;
-
-// first i in [a, p] with r[i] >= x, given the answer is <= p
-__device__ __forceinline__ int lb_back(const uint32_t *__restrict__ r, int a, int p, uint32_t x) {
-  int hi = p, d = 1;
-#pragma unroll
-  for (int s = 0; s < kGallop; ++s) {
-    const int i = hi - d;
-    if (i < a) return lb_u32(r, a, hi, x);
-    if (__ldg(r + i) < x) return lb_u32(r, i + 1, hi, x);
-    hi = i;
-    d <<= 1;
-  }
-  return lb_u32(r, a, hi, x);
-}
-
-// first i in [p, b] with r[i] > x (b if none), given the answer is >= p
-__device__ __forceinline__ int ub_fwd(const uint32_t *__restrict__ r, int p, int b, uint32_t x) {
-  int lo = p, d = 1;
-#pragma unroll
-  for (int s = 0; s < kGallop; ++s) {
-    const int i = lo + d - 1;
-    if (i >= b) return ub_u32(r, lo, b, x);
-    if (__ldg(r + i) > x) return ub_u32(r, lo, i, x);
-    lo = i + 1;
-    d <<= 1;
-  }
-  return ub_u32(r, lo, b, x);
-}
-
-__device__ __forceinline__ Win window_at(const Ctx &c, int dir, int x, int p) {
-#if TM_PIVOT
-  const int a = __ldg(c.g.ptr[dir] + x), b = __ldg(c.g.ptr[dir] + x + 1);
-  return {lb_back(c.g.rnk[dir], a, p, c.lo), ub_fwd(c.g.rnk[dir], p, b, c.hi)};
-#else
-  (void)p;
-  return window(c, dir, x);
-#endif
-}
-
-// the trigger's pivots: its own slots in u's out-run and v's in-run, and the
-// time-aligned slots in u's in-run and v's out-run (indexed like Ctx windows:
-// 0 u-in, 1 u-out, 2 v-in, 3 v-out)
-struct Pivots {
-  int p[4];
-};
-__device__ __forceinline__ Pivots trigger_pivots(const DevGraph &g, int e) {
-  Pivots pv;
-  const int so = __ldg(g.eslot[1] + e), si = __ldg(g.eslot[0] + e);
-  pv.p[1] = so;
-  pv.p[2] = si;
-  pv.p[0] = __ldg(g.tpos[0] + si);
-  pv.p[3] = __ldg(g.tpos[1] + so);
-  return pv;
-}
-
-__device__ __forceinline__ void fill_windows_at(Ctx &c, int need, const Pivots &pv) {
-#if TM_PIVOT
-  c.wui = c.wuo = c.wvi = c.wvo = Win{0, 0};
-  if (need & 1) c.wui = window_at(c, 0, c.u, pv.p[0]);
-  if (need & 2) c.wuo = window_at(c, 1, c.u, pv.p[1]);
-  if (need & 4) c.wvi = window_at(c, 0, c.v, pv.p[2]);
-  if (need & 8) c.wvo = window_at(c, 1, c.v, pv.p[3]);
-#else
-  (void)pv;
-  fill_windows(c, need);
-#endif
-}
-
 // self-loops of x inside the window (kernels.py:279-287): pair run (x, x)
 __device__ __forceinline__ int loops_in_window(const Ctx &c, int x) {
   if (!__ldg(c.g.loop + x)) return 0;

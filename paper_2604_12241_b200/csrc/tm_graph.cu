@@ -135,31 +135,6 @@ __global__ void k_pair_fill(const uint64_t *__restrict__ pair_sorted, const uint
   prev[p] = (q > 0 && pair_sorted[q - 1] == pair_sorted[q]) ? rnk[pids[q - 1]] + 1u : 0u;
 }
 
-// eslot[d][eid[d][p]] = p
-__global__ void k_eslot(const int32_t *__restrict__ eid, int64_t n, int32_t *__restrict__ eslot) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) eslot[eid[p]] = (int32_t)p;
-}
-
-// window pivots of CSR slot p (owner x, nbr n, rank r): the same edge's slot
-// in the other CSR, and the first slot of n's same-direction run at rank >= r
-__global__ void k_pivots(const int32_t *__restrict__ ptr, const int32_t *__restrict__ nbr,
-                         const uint32_t *__restrict__ rnk, const int32_t *__restrict__ eid,
-                         const int32_t *__restrict__ eslot_other, int64_t n,
-                         int32_t *__restrict__ xpos, int32_t *__restrict__ tpos) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  xpos[p] = __ldg(eslot_other + eid[p]);
-  const int m = nbr[p];
-  const uint32_t r = rnk[p];
-  int a = __ldg(ptr + m), b = __ldg(ptr + m + 1);
-  while (a < b) {
-    const int mid = (a + b) >> 1;
-    if (__ldg(rnk + mid) < r) a = mid + 1; else b = mid;
-  }
-  tpos[p] = a;
-}
-
 __global__ void k_max_degree(const int32_t *__restrict__ ptr, int64_t n_nodes,
                              unsigned long long *out) {
   unsigned long long m = 0;
@@ -228,9 +203,6 @@ tmb::DevGraph tm_graph::dev() const {
     g.prev[d] = prev[d].as<uint32_t>();
     g.eid[d] = eid[d].as<int32_t>();
     g.peid[d] = peid[d].as<int32_t>();
-    g.eslot[d] = eslot[d].as<int32_t>();
-    g.xpos[d] = xpos[d].as<int32_t>();
-    g.tpos[d] = tpos[d].as<int32_t>();
   }
   g.loop = loop.as<uint8_t>();
   return g;
@@ -268,8 +240,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
     if ((rc = g->ptr[d].ensure_on(4 * (N + 1), s)) || (rc = g->nbr[d].ensure_on(4 * Ea, s)) ||
         (rc = g->rnk[d].ensure_on(4 * Ea, s)) || (rc = g->eid[d].ensure_on(4 * Ea, s)) ||
         (rc = g->pkey[d].ensure_on(8 * Ea, s)) || (rc = g->prev[d].ensure_on(4 * Ea, s)) ||
-        (rc = g->peid[d].ensure_on(4 * Ea, s)) || (rc = g->eslot[d].ensure_on(4 * Ea, s)) ||
-        (rc = g->xpos[d].ensure_on(4 * Ea, s)) || (rc = g->tpos[d].ensure_on(4 * Ea, s)))
+        (rc = g->peid[d].ensure_on(4 * Ea, s)))
       return rc;
   }
   if (E == 0) {
@@ -371,16 +342,6 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
     TM_CUDA(cudaMemsetAsync(md, 0, 8, s));
     k_max_degree<<<592, kB, 0, s>>>(g->ptr[d].as<int32_t>(), N, md);
     TM_LAUNCHED("k_max_degree");
-    k_eslot<<<grid_for(E, kB), kB, 0, s>>>(g->eid[d].as<int32_t>(), E, g->eslot[d].as<int32_t>());
-    TM_LAUNCHED("k_eslot");
-  }
-  // 5. window pivots (both CSRs and both eslot tables exist now)
-  for (int d = 0; d < 2; ++d) {
-    k_pivots<<<grid_for(E, kB), kB, 0, s>>>(g->ptr[d].as<int32_t>(), g->nbr[d].as<int32_t>(),
-                                            g->rnk[d].as<uint32_t>(), g->eid[d].as<int32_t>(),
-                                            g->eslot[d ^ 1].as<int32_t>(), E, g->xpos[d].as<int32_t>(),
-                                            g->tpos[d].as<int32_t>());
-    TM_LAUNCHED("k_pivots");
   }
   TM_CUDA(cudaStreamSynchronize(s));
   return TM_OK;
@@ -430,8 +391,7 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
   for (const DevBuf *b : {&g->e_src, &g->e_dst, &g->e_rank, &g->uniq_time, &g->loop})
     bytes += (int64_t)b->bytes;
   for (int d = 0; d < 2; ++d)
-    for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d], &g->peid[d],
-                            &g->eslot[d], &g->xpos[d], &g->tpos[d]})
+    for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d], &g->peid[d]})
       bytes += (int64_t)b->bytes;
   g->device_bytes = bytes;
   *out = g;

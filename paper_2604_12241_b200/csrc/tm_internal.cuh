@@ -51,12 +51,6 @@ struct DevGraph {
   const uint32_t *prev[2];
   const int32_t *eid[2];   // edge id per CSR slot (members attribution)
   const int32_t *peid[2];  // edge id per pair slot (members attribution)
-  // window pivots: a slot known to lie inside (or at the edge of) a window,
-  // so window bounds are galloped from it instead of bisecting whole runs
-  const int32_t *eslot[2];  // edge id -> its CSR slot (dir 0: in, 1: out)
-  const int32_t *xpos[2];   // CSR slot -> slot of the same edge in the other CSR
-  const int32_t *tpos[2];   // CSR slot (owner x, nbr n, rank r) -> first slot of
-                            // n's same-direction run with rank >= r
   const uint8_t *loop;
 };
 
@@ -183,7 +177,6 @@ struct tm_graph {
 
   tmb::DevBuf e_src, e_dst, e_rank, uniq_time, loop, maxdeg;
   tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2], peid[2];
-  tmb::DevBuf eslot[2], xpos[2], tpos[2];
 
   // mining scratch (grow-only)
   tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks, split_scratch;

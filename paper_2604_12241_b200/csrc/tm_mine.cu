@@ -106,9 +106,9 @@ __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p
 // distinct-neighbour intersection |N^{dx}(x) ∩ N^{dy}(y)|, early exit at K,
 // walking the shorter windowed slice (sg: x = s out, y = v in; gs: x = d
 // in, y = u out).  x and y are never members (no self-loops).
-__device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int px, int y, int dy,
+__device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, int dy,
                                           const Win &wy, int K) {
-  const Win wx = window_at(c, dx, x, px);
+  const Win wx = window(c, dx, x);
   const bool walk_x = wx.len() <= wy.len();
   const Win w = walk_x ? wx : wy;
   const int other = walk_x ? y : x;
@@ -175,7 +175,7 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
 #pragma unroll
     for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
     if (dup || !first_in_window(c, 1, j)) continue;
-    const Win w = window_at(c, 1, a, __ldg(c.g.tpos[1] + j));  // a's out-window: closes and descends
+    const Win w = window(c, 1, a);  // a's out-window: closes and descends
     if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, w, path), acc);
     if constexpr (L + 1 < MAXD) {
       path[L] = a;
@@ -189,9 +189,9 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
 
 // cycles through chain node a1 = m (a V item), depths 1..maxd
 __device__ __forceinline__ void cycles_from_a1(const Ctx &c, const CycGroup &cg, int row, int grp,
-                                               int m, int pm, CycAcc &acc, const Queue &qu) {
+                                               int m, CycAcc &acc, const Queue &qu) {
   int path[kMaxChain] = {m, -1, -1, -1, -1};
-  const Win w = window_at(c, 1, m, pm);
+  const Win w = window(c, 1, m);
   if (cg.mask & 2) close_at(cg, 1, close_count<0>(c, m, w, path), acc);
   if (cg.maxd < 2) return;
   if (w.len() > kDeepSplit && emit(qu, row, grp, 1, m, -1, -1, -1, -1, w.a, w.b)) return;
@@ -234,7 +234,7 @@ __device__ __forceinline__ void u_item(const Ctx &c, const DevPlans &P, const De
   if ((gr.cyc.mask & 1) && c.u != c.v && exists_in(c, 1, c.v, c.wvo, m)) sk.c3();
   for (int i = 0; i < gr.n_sg; ++i) {  // sg: source m (kernels.py:365-374)
     const int ci = gr.sg_col[i], K = P.p[ci].min_size;
-    if (inner_hits(c, m, 1, __ldg(c.g.xpos[0] + j), c.v, 0, c.wvi, K) >= K) sk.col(ci, 1);
+    if (inner_hits(c, m, 1, c.v, 0, c.wvi, K) >= K) sk.col(ci, 1);
   }
 }
 
@@ -246,13 +246,13 @@ __device__ __forceinline__ void v_item(const Ctx &c, const DevPlans &P, const De
   if (gr.has_stack) sk.sc();
   for (int i = 0; i < gr.n_gs; ++i) {  // gs: destination m (Appendix B)
     const int ci = gr.gs_col[i], K = P.p[ci].min_size;
-    if (inner_hits(c, m, 0, __ldg(c.g.xpos[1] + j), c.u, 1, c.wuo, K) >= K) sk.col(ci, 1);
+    if (inner_hits(c, m, 0, c.u, 1, c.wuo, K) >= K) sk.col(ci, 1);
   }
   if (gr.cyc.maxd >= 1 && c.u != c.v && c.wui.len() > 0) {
     CycAcc acc;
 #pragma unroll
     for (int e = 0; e < kMaxCyc; ++e) acc.e[e] = 0;
-    cycles_from_a1(c, gr.cyc, row, grp, m, __ldg(c.g.tpos[1] + j), acc, qu);
+    cycles_from_a1(c, gr.cyc, row, grp, m, acc, qu);
 #pragma unroll
     for (int e = 0; e < kMaxCyc; ++e)
       if (e < gr.cyc.n && acc.e[e]) sk.col(gr.cyc.col[e], acc.e[e]);
@@ -341,22 +341,18 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
   ws.rowid[lane] = (int)row;
   int u = 0, v = 0;
   uint32_t r = 0;
-  Pivots pv{};
   if (valid) {
     const int e = (int)(lo + row);
     u = __ldg(g.e_src + e);
     v = __ldg(g.e_dst + e);
     r = __ldg(g.e_rank + e);
-#if TM_PIVOT
-    pv = trigger_pivots(g, e);
-#endif
   }
   for (int i = 0; i < C; ++i) stage[lane * C + i] = 0;
 
   for (int gi = 0; gi < P.ngroups; ++gi) {
     const DevGroup &gr = P.gr[gi];
     Ctx c{g, u, v, valid ? __ldg(gr.lo_tab + r) : 1u, r, {}, {}, {}, {}};
-    if (valid) fill_windows_at(c, gr.need, pv);
+    if (valid) fill_windows(c, gr.need);
     // per-lane columns: fan / degree (kernels.py:290-303), cycle_2 (:320-322)
     if (valid) {
       for (int i = 0; i < gr.ncols; ++i) {
@@ -468,11 +464,7 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     const DevGroup &gr = P.gr[t.grp];
     const uint32_t r = __ldg(g.e_rank + e);
     Ctx c{g, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {}};
-#if TM_PIVOT
-    fill_windows_at(c, gr.need, trigger_pivots(g, e));
-#else
     fill_windows(c, gr.need);
-#endif
     long long *orow = out + (int64_t)t.row * P.n;
     if (t.level == kLvlDomU || t.level == kLvlDomV) {
       GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
