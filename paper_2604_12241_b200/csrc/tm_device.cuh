@@ -8,6 +8,24 @@
 namespace tmb {
 namespace dev {
 
+// Work counters for tools/work_profile.py (build with -DTM_COUNTERS=1; a
+// no-op otherwise).  Each translation unit has its own copy.
+#ifndef TM_COUNTERS
+#define TM_COUNTERS 0
+#endif
+enum CtrId {
+  kCtrTrig, kCtrUWalk, kCtrUItem, kCtrVWalk, kCtrVItem, kCtrWin, kCtrBisect32, kCtrScanCall,
+  kCtrScanLoad, kCtrPairCall, kCtrBisect64, kCtrInnerCall, kCtrInnerWalk, kCtrChain1, kCtrChain2,
+  kCtrChain3, kCtrChain4, kCtrCloseCall, kCtrCloseWalk, kCtrDomTask, kCtrChainTask, kCtrFirst,
+  kCtrInnerSkip, kCtrUSkip, kCtrVSkip, kCtrN
+};
+#if TM_COUNTERS
+static __device__ unsigned long long tm_ctr[kCtrN];
+#define TM_CNT(i, n) atomicAdd(&::tmb::dev::tm_ctr[(i)], (unsigned long long)(n))
+#else
+#define TM_CNT(i, n) ((void)0)
+#endif
+
 struct Win {
   int a, b;
   __device__ __forceinline__ int len() const { return b - a; }
@@ -15,6 +33,7 @@ struct Win {
 
 __device__ __forceinline__ int lb_u32(const uint32_t *__restrict__ r, int a, int b, uint32_t x) {
   while (a < b) {
+    TM_CNT(kCtrBisect32, 1);
     int m = (a + b) >> 1;
     if (__ldg(r + m) < x) a = m + 1; else b = m;
   }
@@ -22,6 +41,7 @@ __device__ __forceinline__ int lb_u32(const uint32_t *__restrict__ r, int a, int
 }
 __device__ __forceinline__ int ub_u32(const uint32_t *__restrict__ r, int a, int b, uint32_t x) {
   while (a < b) {
+    TM_CNT(kCtrBisect32, 1);
     int m = (a + b) >> 1;
     if (__ldg(r + m) <= x) a = m + 1; else b = m;
   }
@@ -29,6 +49,7 @@ __device__ __forceinline__ int ub_u32(const uint32_t *__restrict__ r, int a, int
 }
 __device__ __forceinline__ int lb_u64(const uint64_t *__restrict__ k, int a, int b, uint64_t x) {
   while (a < b) {
+    TM_CNT(kCtrBisect64, 1);
     int m = (a + b) >> 1;
     if (__ldg(k + m) < x) a = m + 1; else b = m;
   }
@@ -65,6 +86,7 @@ __device__ __forceinline__ int ub_gallop(const uint32_t *__restrict__ r, int s, 
 
 // windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
 __device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
+  TM_CNT(kCtrWin, 1);
   const int a = __ldg(c.g.ptr[dir] + x), b = __ldg(c.g.ptr[dir] + x + 1);
   const int wa = lb_u32(c.g.rnk[dir], a, b, c.lo);
 #if TM_UB_GALLOP
@@ -124,6 +146,7 @@ __device__ __forceinline__ int loops_in_window(const Ctx &c, int x) {
 // (np.unique, kernels.py:59): the previous entry with the same (owner, nbr)
 // lies before lo (prev = rank + 1, 0 = none)
 __device__ __forceinline__ bool first_in_window(const Ctx &c, int dir, int j) {
+  TM_CNT(kCtrFirst, 1);
   return __ldg(c.g.prev[dir] + j) <= c.lo;
 }
 
@@ -132,13 +155,12 @@ __device__ __forceinline__ bool first_in_window(const Ctx &c, int dir, int j) {
 // SHORTER pair run: x's dir run keyed by n, or n's opposite run keyed by x
 // (n in N^dir(x)  <=>  x in N^{1-dir}(n)).
 constexpr int kScanWin = 16;
-__device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
-  if (w.len() <= kScanWin) {
-    bool hit = false;
-    for (int j = w.a; j < w.b && !hit; ++j) hit = __ldg(c.g.nbr[dir] + j) == n;
-    return hit;
-  }
-  const int xs = __ldg(c.g.ptr[dir] + x), xe = __ldg(c.g.ptr[dir] + x + 1);
+
+// is n in x's dir-window?  x's run is [xs, xe): one bisection of the SHORTER
+// pair run — x's dir run keyed by n, or n's opposite run keyed by x
+// (n in N^dir(x)  <=>  x in N^{1-dir}(n)).  Needs no window of x.
+__device__ __forceinline__ bool exists_pair(const Ctx &c, int dir, int x, int xs, int xe, int n) {
+  TM_CNT(kCtrPairCall, 1);
   const int ns = __ldg(c.g.ptr[dir ^ 1] + n), ne = __ldg(c.g.ptr[dir ^ 1] + n + 1);
   const bool from_x = xe - xs <= ne - ns;
   const uint64_t *k = c.g.pkey[from_x ? dir : dir ^ 1];
@@ -146,6 +168,21 @@ __device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Wi
   const uint64_t base = (uint64_t)(uint32_t)(from_x ? n : x) << c.g.rank_bits;
   const int q = lb_u64(k, s, e, base + c.lo);
   return q < e && __ldg(k + q) <= base + c.hi;
+}
+
+// does x's dir-window w contain neighbour n?  Windows are time-local and
+// short: scan them.  A wide w (a hub) is answered from the pair index.
+__device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
+  if (w.len() <= kScanWin) {
+    TM_CNT(kCtrScanCall, 1);
+    bool hit = false;
+    for (int j = w.a; j < w.b && !hit; ++j) {
+      TM_CNT(kCtrScanLoad, 1);
+      hit = __ldg(c.g.nbr[dir] + j) == n;
+    }
+    return hit;
+  }
+  return exists_pair(c, dir, x, __ldg(c.g.ptr[dir] + x), __ldg(c.g.ptr[dir] + x + 1), n);
 }
 
 __device__ __forceinline__ long long warp_sum(long long x) {

@@ -79,6 +79,9 @@ struct CycGroup {
 // lower-bound table, one pass over each trigger slice
 struct DevGroup {
   const uint32_t *lo_tab;  // rank -> first rank with time >= uniq_time[rank] - delta
+  // own windows by edge id (or null): own[1][e] = window of e's source
+  // out-run at e's time (u-out), own[0][e] = of e's destination in-run (v-in)
+  const int2 *own[2];
   int32_t need;            // trigger windows (1 u-in, 2 u-out, 4 v-in, 8 v-out)
   int32_t udom, vdom;      // N-(u) / N+(v) item passes needed
   int32_t has_stack;
@@ -179,7 +182,7 @@ struct tm_graph {
   tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2], peid[2];
 
   // mining scratch (grow-only)
-  tmb::DevBuf lo_tabs, heavy_q, heavy_n, out_scratch, tasks, split_scratch;
+  tmb::DevBuf lo_tabs, own_tabs, heavy_q, heavy_n, out_scratch, tasks, split_scratch;
   tmb::DevBuf csv_buf;  // formatted feature CSV (tm_csv_format)
   int64_t csv_bytes = 0;
   tmb::DevBuf inst_buf;  // instance records (tm_collect_instances, tm_vm_collect)

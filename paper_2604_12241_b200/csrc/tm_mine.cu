@@ -82,6 +82,7 @@ struct Queue {
 __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p1, int p2, int p3,
                      int p4, int a, int b) {
   const int n = (b - a + kTaskSpan - 1) / kTaskSpan;
+  TM_CNT(level >= kLvlDomU ? kCtrDomTask : kCtrChainTask, n);
   const int base = atomicAdd(qu.count, n);
   if (base + n > qu.cap) {
     for (int k = base; k < qu.cap; ++k) qu.q[k].row = -1;  // holes stay empty
@@ -103,21 +104,46 @@ __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p
 
 // ------------------------------------------------------------ set helpers
 
-// distinct-neighbour intersection |N^{dx}(x) ∩ N^{dy}(y)|, early exit at K,
-// walking the shorter windowed slice (sg: x = s out, y = v in; gs: x = d
-// in, y = u out).  x and y are never members (no self-loops).
+// distinct-neighbour intersection |N^{dx}(x) ∩ N^{dy}(y)| \ {x, y}, early
+// exit at K (sg: x = s out, y = v in; gs: x = d in, y = u out).  x and y are
+// never members (no self-loops).  f >= 0 is a node known to be in the
+// intersection and not in {x, y} (sg: u, gs: v, when u != v — the trigger
+// and the item edge put it there): it counts without a probe and the walks
+// skip it.  Since f is one of y's window entries, no more than wy.len()
+// nodes can hit, which often settles the column before x's window is read.
+// A wide run of x (a sender hub) is not bisected when y's window is short:
+// y's side is walked and each node probed in the pair index instead.
+constexpr int kLazyRun = 32;
 __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, int dy,
-                                          const Win &wy, int K) {
-  const Win wx = window(c, dx, x);
+                                          const Win &wy, int K, int f) {
+  int hits = f >= 0 ? 1 : 0;
+  TM_CNT(kCtrInnerCall, 1);
+  if (hits >= K || wy.len() < K) {
+    TM_CNT(kCtrInnerSkip, 1);
+    return hits;
+  }
+  const int xs = __ldg(c.g.ptr[dx] + x), xe = __ldg(c.g.ptr[dx] + x + 1);
+  if (xe - xs > kLazyRun && wy.len() <= kLazyRun) {
+    for (int j = wy.a; j < wy.b && hits < K; ++j) {
+      TM_CNT(kCtrInnerWalk, 1);
+      const int m = __ldg(c.g.nbr[dy] + j);
+      if (m == x || m == y || m == f || !first_in_window(c, dy, j)) continue;
+      hits += exists_pair(c, dx, x, xs, xe, m);
+    }
+    return hits;
+  }
+  const int wa = lb_u32(c.g.rnk[dx], xs, xe, c.lo);
+  const Win wx{wa, ub_u32(c.g.rnk[dx], wa, xe, c.hi)};
+  TM_CNT(kCtrWin, 1);
   const bool walk_x = wx.len() <= wy.len();
   const Win w = walk_x ? wx : wy;
   const int other = walk_x ? y : x;
   const int d = walk_x ? dx : dy, od = walk_x ? dy : dx;
   const Win ow = walk_x ? wy : wx;
-  int hits = 0;
   for (int j = w.a; j < w.b && hits < K; ++j) {
+    TM_CNT(kCtrInnerWalk, 1);
     const int m = __ldg(c.g.nbr[d] + j);
-    if (m == x || m == y || !first_in_window(c, d, j)) continue;
+    if (m == x || m == y || m == f || !first_in_window(c, d, j)) continue;
     hits += exists_in(c, od, other, ow, m);
   }
   return hits;
@@ -133,7 +159,9 @@ __device__ __forceinline__ int close_count(const Ctx &c, int a, const Win &wa,
   const Win w = walk_a ? wa : c.wui;
   const int d = walk_a ? 1 : 0;
   int cnt = 0;
+  TM_CNT(kCtrCloseCall, 1);
   for (int j = w.a; j < w.b; ++j) {
+    TM_CNT(kCtrCloseWalk, 1);
     const int m = __ldg(c.g.nbr[d] + j);
     if (m == a || m == c.u || m == c.v) continue;
     bool dup = false;
@@ -175,6 +203,7 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
 #pragma unroll
     for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
     if (dup || !first_in_window(c, 1, j)) continue;
+    TM_CNT(kCtrChain1 + L, 1);
     const Win w = window(c, 1, a);  // a's out-window: closes and descends
     if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, w, path), acc);
     if constexpr (L + 1 < MAXD) {
@@ -229,12 +258,14 @@ template <class Sink>
 __device__ __forceinline__ void u_item(const Ctx &c, const DevPlans &P, const DevGroup &gr, int j,
                                        Sink &sk) {
   const int m = __ldg(c.g.nbr[0] + j);
+  TM_CNT(kCtrUWalk, 1);
   if (m == c.u || m == c.v || !first_in_window(c, 0, j)) return;
+  TM_CNT(kCtrUItem, 1);
   if (gr.has_stack) sk.sa();
   if ((gr.cyc.mask & 1) && c.u != c.v && exists_in(c, 1, c.v, c.wvo, m)) sk.c3();
   for (int i = 0; i < gr.n_sg; ++i) {  // sg: source m (kernels.py:365-374)
     const int ci = gr.sg_col[i], K = P.p[ci].min_size;
-    if (inner_hits(c, m, 1, c.v, 0, c.wvi, K) >= K) sk.col(ci, 1);
+    if (inner_hits(c, m, 1, c.v, 0, c.wvi, K, c.u != c.v ? c.u : -1) >= K) sk.col(ci, 1);
   }
 }
 
@@ -242,11 +273,13 @@ template <class Sink>
 __device__ __forceinline__ void v_item(const Ctx &c, const DevPlans &P, const DevGroup &gr, int grp,
                                        int row, int j, Sink &sk, const Queue &qu) {
   const int m = __ldg(c.g.nbr[1] + j);
+  TM_CNT(kCtrVWalk, 1);
   if (m == c.u || m == c.v || !first_in_window(c, 1, j)) return;
+  TM_CNT(kCtrVItem, 1);
   if (gr.has_stack) sk.sc();
   for (int i = 0; i < gr.n_gs; ++i) {  // gs: destination m (Appendix B)
     const int ci = gr.gs_col[i], K = P.p[ci].min_size;
-    if (inner_hits(c, m, 0, c.u, 1, c.wuo, K) >= K) sk.col(ci, 1);
+    if (inner_hits(c, m, 0, c.u, 1, c.wuo, K, c.u != c.v ? c.v : -1) >= K) sk.col(ci, 1);
   }
   if (gr.cyc.maxd >= 1 && c.u != c.v && c.wui.len() > 0) {
     CycAcc acc;
@@ -256,6 +289,22 @@ __device__ __forceinline__ void v_item(const Ctx &c, const DevPlans &P, const De
 #pragma unroll
     for (int e = 0; e < kMaxCyc; ++e)
       if (e < gr.cyc.n && acc.e[e]) sk.col(gr.cyc.col[e], acc.e[e]);
+  }
+}
+
+// the trigger's windows: own windows from the group's tables, the rest bisected
+__device__ __forceinline__ void trigger_windows(Ctx &c, const DevGroup &gr, int e) {
+  int need = gr.need;
+  if (gr.own[1]) need &= ~2;
+  if (gr.own[0]) need &= ~4;
+  fill_windows(c, need);
+  if (gr.own[1] && (gr.need & 2)) {
+    const int2 w = __ldg(gr.own[1] + e);
+    c.wuo = Win{w.x, w.y};
+  }
+  if (gr.own[0] && (gr.need & 4)) {
+    const int2 w = __ldg(gr.own[0] + e);
+    c.wvi = Win{w.x, w.y};
   }
 }
 
@@ -348,11 +397,12 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     r = __ldg(g.e_rank + e);
   }
   for (int i = 0; i < C; ++i) stage[lane * C + i] = 0;
+  if (valid) TM_CNT(kCtrTrig, 1);
 
   for (int gi = 0; gi < P.ngroups; ++gi) {
     const DevGroup &gr = P.gr[gi];
     Ctx c{g, u, v, valid ? __ldg(gr.lo_tab + r) : 1u, r, {}, {}, {}, {}};
-    if (valid) fill_windows(c, gr.need);
+    if (valid) trigger_windows(c, gr, (int)row);
     // per-lane columns: fan / degree (kernels.py:290-303), cycle_2 (:320-322)
     if (valid) {
       for (int i = 0; i < gr.ncols; ++i) {
@@ -464,7 +514,7 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     const DevGroup &gr = P.gr[t.grp];
     const uint32_t r = __ldg(g.e_rank + e);
     Ctx c{g, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {}};
-    fill_windows(c, gr.need);
+    trigger_windows(c, gr, t.row);
     long long *orow = out + (int64_t)t.row * P.n;
     if (t.level == kLvlDomU || t.level == kLvlDomV) {
       GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
@@ -528,6 +578,27 @@ __global__ void k_lo_table(const int64_t *__restrict__ uniq, int64_t R, long lon
   lo_tab[r] = (uint32_t)a;
 }
 
+// own-window table of CSR direction dir: slot p of owner x (edge e = eid[p])
+// is inside x's window at e's own time, so that window's lower bound is
+// searched in [a, p] only and its upper bound galloped forward from p.
+// Consecutive slots share their search paths (one run, nearby targets), so
+// the bisections of a hub run are L1 broadcasts instead of the dependent
+// DRAM chains the trigger would otherwise walk.  Written by edge id: the
+// trigger kernels read it coalesced.
+__global__ void k_own_windows(const __grid_constant__ DevGraph g, const uint32_t *__restrict__ lo_tab,
+                              int dir, int64_t lo, int64_t hi, int2 *__restrict__ tab) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= g.n_edges) return;
+  const int e = __ldg(g.eid[dir] + p);
+  if (e < lo || e >= hi) return;
+  const int x = dir ? __ldg(g.e_src + e) : __ldg(g.e_dst + e);
+  const int a = __ldg(g.ptr[dir] + x), b = __ldg(g.ptr[dir] + x + 1);
+  const uint32_t *rk = g.rnk[dir];
+  const uint32_t r = __ldg(rk + p);
+  const int lb = lb_u32(rk, a, (int)p, __ldg(lo_tab + r));
+  tab[e - lo] = make_int2(lb, ub_gallop(rk, (int)p + 1, b, r));
+}
+
 }  // namespace
 }  // namespace tmb
 
@@ -539,6 +610,15 @@ static bool source_order() {
   static bool on = [] {
     const char *e = getenv("TM_ORDER");
     return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// TM_OWN=0 turns the own-window tables off (A/B)
+static bool own_windows_enabled() {
+  static bool on = [] {
+    const char *e = getenv("TM_OWN");
+    return !(e && e[0] == '0');
   }();
   return on;
 }
@@ -620,12 +700,28 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   const int64_t R = g->n_ranks;
   int rc;
   if ((rc = g->lo_tabs.ensure(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups))) return rc;
+  // own-window tables pay off when a group needs them for many triggers
+  const int64_t E = g->n_edges;
+  const bool own_on = own_windows_enabled() && rows * 64 >= E;
+  int n_own = 0;
+  if (own_on)
+    for (int k = 0; k < dp.ngroups; ++k) n_own += ((dp.gr[k].need >> 1) & 1) + ((dp.gr[k].need >> 2) & 1);
+  if (n_own && (rc = g->own_tabs.ensure(sizeof(int2) * (size_t)rows * n_own))) return rc;
+  const DevGraph dg = g->dev();
   int rounds = 0;
+  int own_i = 0;
   for (int k = 0; k < dp.ngroups; ++k) {
     dp.gr[k].lo_tab = g->lo_tabs.as<uint32_t>() + (size_t)k * R;
     k_lo_table<<<grid_for(R, 256), 256, 0, s>>>(g->uniq_time.as<int64_t>(), R, deltas[k],
                                                 g->lo_tabs.as<uint32_t>() + (size_t)k * R);
     TM_LAUNCHED("k_lo_table");
+    for (int dir = 0; dir < 2 && own_on; ++dir) {
+      if (!((dp.gr[k].need >> (dir ? 1 : 2)) & 1)) continue;
+      int2 *tab = g->own_tabs.as<int2>() + (size_t)rows * own_i++;
+      k_own_windows<<<grid_for(E, 256), 256, 0, s>>>(dg, dp.gr[k].lo_tab, dir, lo, hi, tab);
+      TM_LAUNCHED("k_own_windows");
+      dp.gr[k].own[dir] = tab;
+    }
     // task rounds: domain tasks, then one per chain level below a1
     if (dp.gr[k].udom || dp.gr[k].vdom)
       rounds = std::max(rounds, 1 + std::max(0, dp.gr[k].cyc.maxd - 1));
@@ -650,7 +746,6 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   Queue qa{g->tasks.as<Task>(), cnt + 1, (int32_t)task_cap};
   Queue qb{g->tasks.as<Task>() + task_cap, cnt + 2, (int32_t)task_cap};
 
-  const DevGraph dg = g->dev();
   const size_t smem = sizeof(long long) * kThreads * n_plans;
   if (smem > 48 * 1024)
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -681,18 +776,22 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     const int64_t r0 = std::min<int64_t>(rows, pc * per), r1 = std::min<int64_t>(rows, r0 + per);
     long long *po = d_out + r0 * n_plans;
     Queue a = qa, b = qb;
+    DevPlans dpp = dp;  // own-window tables are indexed relative to the piece
+    for (int k = 0; k < dpp.ngroups; ++k)
+      for (int d = 0; d < 2; ++d)
+        if (dpp.gr[k].own[d]) dpp.gr[k].own[d] += r0;
     TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
     // full-range device-output calls process triggers in out-CSR order
     const int32_t *order = (pieces == 1 && lo == 0 && hi == g->n_edges && source_order())
                                ? g->eid[1].as<int32_t>() : nullptr;
     k_mine_warp<<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
-        dg, dp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt,
+        dg, dpp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt,
         g->split_scratch.as<int32_t>(), (int32_t)split_cap, order);
     TM_LAUNCHED("k_mine_warp");
     if (g->prof && pc == pieces - 1) TM_CUDA(cudaEventRecord(g->ev[1], s));
     for (int r = 0; r < rounds; ++r) {
       TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int32_t), s));
-      k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dp, lo + r0, po,
+      k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po,
                                                       g->split_scratch.as<int32_t>(), a, b);
       TM_LAUNCHED("k_mine_tasks");
       std::swap(a, b);
@@ -725,6 +824,24 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   }
   g->last.kernel_launches = tm_kernel_launch_count() - launches0;
   return TM_OK;
+}
+
+// diagnostic: work counters of the mining kernels (-DTM_COUNTERS=1 builds;
+// tools/work_profile.py).  Not part of the public header.
+extern "C" int tm_debug_counters(int reset, int64_t *out, int n) {
+#if TM_COUNTERS
+  unsigned long long h[kCtrN] = {};
+  TM_CUDA(cudaMemcpyFromSymbol(h, dev::tm_ctr, sizeof(h)));
+  for (int i = 0; i < n && i < kCtrN; ++i) out[i] = (int64_t)h[i];
+  if (reset) {
+    unsigned long long z[kCtrN] = {};
+    TM_CUDA(cudaMemcpyToSymbol(dev::tm_ctr, z, sizeof(z)));
+  }
+  return kCtrN;
+#else
+  (void)reset; (void)out; (void)n;
+  return 0;
+#endif
 }
 
 extern "C" int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats) {
