@@ -56,6 +56,7 @@ constexpr int kDomSplit = 256;       // a trigger slice above this becomes domai
 constexpr int kDeepSplit = 64;       // chain nodes with wider windows become chain tasks
 constexpr int kTaskSpan = 128;       // entries per task (4 per lane)
 constexpr int kLvlDomU = 8, kLvlDomV = 9;  // Task::level of domain tasks
+constexpr int kPullFlag = 32;  // Task::level bit: a whole wide window to expand backwards (pull_task)
 constexpr int kHostPieces = 4;     // host-output pieces overlapped with their D2H
 
 using namespace dev;
@@ -99,6 +100,25 @@ __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p
     t.path[0] = p0; t.path[1] = p1; t.path[2] = p2; t.path[3] = p3; t.path[4] = p4;
     qu.q[base + k] = t;
   }
+  return true;
+}
+
+// one task for the whole range [a, b) (a pull task): false when the queue is full
+__device__ bool emit_whole(const Queue &qu, int row, int grp, int level, const int (&path)[kMaxChain],
+                           int a, int b) {
+  const int k = atomicAdd(qu.count, 1);
+  TM_CNT(kCtrChainTask, 1);
+  if (k >= qu.cap) return false;
+  Task t;
+  t.row = row;
+  t.grp = (int8_t)grp;
+  t.level = (int8_t)level;
+  t.pad0 = t.pad1 = 0;
+  t.a = a;
+  t.b = b;
+#pragma unroll
+  for (int i = 0; i < kMaxChain; ++i) t.path[i] = path[i];
+  qu.q[k] = t;
   return true;
 }
 
@@ -190,8 +210,42 @@ __device__ __forceinline__ void close_at(const CycGroup &cg, int d, int cc, CycA
 //   cycle_{d+3} closes at depth d.
 // Level L walks entries j in [ja, jb) of the out-slice of a_L = path[L-1]
 // (L >= 1; level 0 is the V item loop) choosing a_{L+1}.  A chosen node
-// whose window exceeds kDeepSplit is emitted as a chain task when possible.
-template <int MAXD, int L>
+// whose window exceeds kDeepSplit is expanded backwards (pull_level) when
+// the trigger's backward sets are small, else emitted as a chain task.
+template <int MAXD, int L, bool PI>
+__device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                            int (&path)[kMaxChain], int ja, int jb, CycAcc &acc,
+                                            const Queue &qu);
+template <int MAXD, int J, bool PI>
+__device__ __forceinline__ bool pull_level(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                           int (&path)[kMaxChain], const Win &ow, CycAcc &acc,
+                                           const Queue &qu);
+
+// a_{L+1} = a chosen (all exclusions checked): close at depth L + 1, descend.
+// PI: expand wide nodes backwards in place (task kernel); otherwise hand the
+// whole window to a pull task, keeping the warp kernel's walkers lean.
+template <int MAXD, int L, bool PI>
+__device__ __forceinline__ void chain_pick(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                           int (&path)[kMaxChain], int a, CycAcc &acc,
+                                           const Queue &qu) {
+  TM_CNT(kCtrChain1 + L, 1);
+  const Win w = window(c, 1, a);  // a's out-window: closes and descends
+  if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, w, path), acc);
+  if constexpr (L + 1 < MAXD) {
+    path[L] = a;
+    if (w.len() > kDeepSplit) {
+      if constexpr (PI) {
+        if (pull_level<MAXD, L + 2, PI>(c, cg, row, grp, path, w, acc, qu)) return;
+        if (emit(qu, row, grp, L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b)) return;
+      } else {
+        if (emit_whole(qu, row, grp, (L + 1) | kPullFlag, path, w.a, w.b)) return;
+      }
+    }
+    chain_level<MAXD, L + 1, PI>(c, cg, row, grp, path, w.a, w.b, acc, qu);
+  }
+}
+
+template <int MAXD, int L, bool PI>
 __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
                                             int (&path)[kMaxChain], int ja, int jb, CycAcc &acc,
                                             const Queue &qu) {
@@ -203,32 +257,118 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
 #pragma unroll
     for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
     if (dup || !first_in_window(c, 1, j)) continue;
-    TM_CNT(kCtrChain1 + L, 1);
-    const Win w = window(c, 1, a);  // a's out-window: closes and descends
-    if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, w, path), acc);
-    if constexpr (L + 1 < MAXD) {
-      path[L] = a;
-      if (w.len() > kDeepSplit &&
-          emit(qu, row, grp, L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b))
-        continue;
-      chain_level<MAXD, L + 1>(c, cg, row, grp, path, w.a, w.b, acc, qu);
-    }
+    chain_pick<MAXD, L, PI>(c, cg, row, grp, path, a, acc, qu);
   }
 }
 
+// Backward expansion for a wide chain node (a sender hub).  Every chain
+// that contributes reaches u through the window: a node at depth j closing
+// at depth d >= j lies in B_{2+d-j}, where B_1 = N-(u) \ {u, v} and
+// B_{k+1} = N-(B_k) \ {u, v} (windowed, distinct).  These sets are
+// supersets of the useful choices — pruning with them skips only chains
+// that add nothing — and they are small when in-degrees are, so the hub's
+// window is not walked: each useful node b is probed for owner -> b in the
+// pair index and, if present, picked exactly as the walk would pick it.
+// Declines (returns false) when a set overflows or is not much smaller than
+// the window; the caller then walks or emits tasks as before.
+constexpr int kBCap = 48;
+__device__ __forceinline__ bool bset_add(int *node, int from, int &n, int m) {
+  for (int i = from; i < n; ++i)
+    if (node[i] == m) return true;
+  if (n == kBCap) return false;
+  node[n++] = m;
+  return true;
+}
+
+// the useful depth-J nodes (layers 2 + d - J for the closing depths d >= J
+// in mask), or -1 when a set overflows.  Out of line: it runs for wide
+// chain nodes only and keeps its arrays off the walkers' registers.
+__device__ __noinline__ int useful_nodes(const DevGraph &g, int u, int v, uint32_t lo, uint32_t hi,
+                                         int wa, int wb, int mask, int maxd, int J, int *use) {
+  const Ctx c{g, u, v, lo, hi, {wa, wb}, {}, {}, {}};
+  const int H = 2 + maxd - J;  // deepest layer any useful depth-J node can be in
+  int node[kBCap], lend[kMaxChain + 3];
+  int n = 0;
+  lend[0] = 0;
+  for (int j = wa; j < wb; ++j) {  // B_1
+    const int m = __ldg(g.nbr[0] + j);
+    if (m == u || m == v || !first_in_window(c, 0, j)) continue;
+    if (!bset_add(node, 0, n, m)) return -1;
+  }
+  lend[1] = n;
+  for (int k = 2; k <= H; ++k) {
+    for (int i = lend[k - 2]; i < lend[k - 1]; ++i) {
+      const Win w = window(c, 0, node[i]);
+      if (w.len() > kBCap) return -1;
+      for (int j = w.a; j < w.b; ++j) {
+        const int m = __ldg(g.nbr[0] + j);
+        if (m == u || m == v || !first_in_window(c, 0, j)) continue;
+        if (!bset_add(node, lend[k - 1], n, m)) return -1;
+      }
+    }
+    lend[k] = n;
+  }
+  int nu = 0;
+  for (int d = J; d <= maxd; ++d) {
+    if (!(mask & (1 << d))) continue;
+    const int k = 2 + d - J;
+    for (int i = lend[k - 1]; i < lend[k]; ++i)
+      if (!bset_add(use, 0, nu, node[i])) return -1;
+  }
+  return nu;
+}
+
+template <int MAXD, int J, bool PI>
+__device__ __forceinline__ bool pull_level(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                           int (&path)[kMaxChain], const Win &ow, CycAcc &acc,
+                                           const Queue &qu) {
+  static_assert(J >= 2 && J <= MAXD, "pull_level depth");
+  int use[kBCap];
+  const int nu = useful_nodes(c.g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, MAXD, J, use);
+  if (nu < 0 || nu * 4 > ow.len()) return false;
+  TM_CNT(kCtrVSkip, 1);
+  const int owner = path[J - 2];
+  const int os = __ldg(c.g.ptr[1] + owner), oe = __ldg(c.g.ptr[1] + owner + 1);
+  for (int i = 0; i < nu; ++i) {
+    const int a = use[i];
+    if (a == owner || a == c.u || a == c.v) continue;
+    bool dup = false;
+#pragma unroll
+    for (int q = 0; q + 2 < J; ++q) dup |= (path[q] == a);
+    if (dup || !exists_pair(c, 1, owner, os, oe, a)) continue;
+    chain_pick<MAXD, J - 1, PI>(c, cg, row, grp, path, a, acc, qu);
+  }
+  return true;
+}
+
 // cycles through chain node a1 = m (a V item), depths 1..maxd
+template <int MAXD, bool PI>
+__device__ __forceinline__ void cycles_a1(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                          int (&path)[kMaxChain], const Win &w, CycAcc &acc,
+                                          const Queue &qu) {
+  if (w.len() > kDeepSplit) {
+    if constexpr (PI) {
+      if (pull_level<MAXD, 2, PI>(c, cg, row, grp, path, w, acc, qu)) return;
+      if (emit(qu, row, grp, 1, path[0], -1, -1, -1, -1, w.a, w.b)) return;
+    } else {
+      if (emit_whole(qu, row, grp, 1 | kPullFlag, path, w.a, w.b)) return;
+    }
+  }
+  chain_level<MAXD, 1, PI>(c, cg, row, grp, path, w.a, w.b, acc, qu);
+}
+
+template <bool PI>
 __device__ __forceinline__ void cycles_from_a1(const Ctx &c, const CycGroup &cg, int row, int grp,
                                                int m, CycAcc &acc, const Queue &qu) {
   int path[kMaxChain] = {m, -1, -1, -1, -1};
   const Win w = window(c, 1, m);
   if (cg.mask & 2) close_at(cg, 1, close_count<0>(c, m, w, path), acc);
-  if (cg.maxd < 2) return;
-  if (w.len() > kDeepSplit && emit(qu, row, grp, 1, m, -1, -1, -1, -1, w.a, w.b)) return;
   switch (cg.maxd) {
-    case 2: chain_level<2, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
-    case 3: chain_level<3, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
-    case 4: chain_level<4, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
-    default: chain_level<5, 1>(c, cg, row, grp, path, w.a, w.b, acc, qu); break;
+    case 0: case 1: return;
+    case 2: cycles_a1<2, PI>(c, cg, row, grp, path, w, acc, qu); break;
+    case 3: cycles_a1<3, PI>(c, cg, row, grp, path, w, acc, qu); break;
+    case 4: cycles_a1<4, PI>(c, cg, row, grp, path, w, acc, qu); break;
+    default: cycles_a1<5, PI>(c, cg, row, grp, path, w, acc, qu); break;
   }
 }
 
@@ -239,7 +379,7 @@ __device__ __forceinline__ void cycles_resume(const Ctx &c, const CycGroup &cg, 
   int path[kMaxChain] = {p0[0], p0[1], p0[2], p0[3], p0[4]};
   switch (cg.maxd * 8 + L) {
 #define TM_CHAIN_CASE(D_, L_) \
-  case D_ * 8 + L_: chain_level<D_, L_>(c, cg, row, grp, path, ja, jb, acc, qu); return;
+  case D_ * 8 + L_: chain_level<D_, L_, true>(c, cg, row, grp, path, ja, jb, acc, qu); return;
     TM_CHAIN_CASE(2, 1)
     TM_CHAIN_CASE(3, 1) TM_CHAIN_CASE(3, 2)
     TM_CHAIN_CASE(4, 1) TM_CHAIN_CASE(4, 2) TM_CHAIN_CASE(4, 3)
@@ -269,7 +409,7 @@ __device__ __forceinline__ void u_item(const Ctx &c, const DevPlans &P, const De
   }
 }
 
-template <class Sink>
+template <bool PI, class Sink>
 __device__ __forceinline__ void v_item(const Ctx &c, const DevPlans &P, const DevGroup &gr, int grp,
                                        int row, int j, Sink &sk, const Queue &qu) {
   const int m = __ldg(c.g.nbr[1] + j);
@@ -285,7 +425,7 @@ __device__ __forceinline__ void v_item(const Ctx &c, const DevPlans &P, const De
     CycAcc acc;
 #pragma unroll
     for (int e = 0; e < kMaxCyc; ++e) acc.e[e] = 0;
-    cycles_from_a1(c, gr.cyc, row, grp, m, acc, qu);
+    cycles_from_a1<PI>(c, gr.cyc, row, grp, m, acc, qu);
 #pragma unroll
     for (int e = 0; e < kMaxCyc; ++e)
       if (e < gr.cyc.n && acc.e[e]) sk.col(gr.cyc.col[e], acc.e[e]);
@@ -455,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     flat_for(ws, lane, vlen, [&](int o, int k) {
       const Ctx co = ctx_of(g, ws, o);
       SmemSink sk{ws, stage, o, C};
-      v_item(co, P, gr, gi, ws.rowid[o], co.wvo.a + k, sk, qu);
+      v_item<false>(co, P, gr, gi, ws.rowid[o], co.wvo.a + k, sk, qu);
     });
     // whole-count columns: stack a * c (kernels.py:379-402), cycle_3 threshold
     if (valid) {
@@ -490,6 +630,53 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
 
 // ------------------------------------------------------------ tasks
 
+// a pull task: owner a_L = path[L-1] with the whole wide window [t.a, t.b);
+// the warp expands it backwards (every lane builds the same sets — uniform
+// loads — then the lanes share the useful nodes), or, when the sets decline,
+// splits it into chain tasks for the next round (walks it when that queue is
+// full).
+template <int MAXD, int L>
+__device__ __forceinline__ void pull_task(const Ctx &c, const CycGroup &cg, const Task &t, int lane,
+                                          CycAcc &acc, const Queue &next) {
+  int path[kMaxChain] = {t.path[0], t.path[1], t.path[2], t.path[3], t.path[4]};
+  int use[kBCap];
+  const int nu = useful_nodes(c.g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, MAXD, L + 1, use);
+  if (nu < 0 || nu * 4 > t.b - t.a) {
+    bool ok = false;
+    if (lane == 0) ok = emit(next, t.row, t.grp, L, path[0], path[1], path[2], path[3], path[4], t.a, t.b);
+    if (__shfl_sync(0xffffffffu, ok, 0)) return;
+    for (int j = t.a + lane; j < t.b; j += 32)
+      chain_level<MAXD, L, true>(c, cg, t.row, t.grp, path, j, j + 1, acc, next);
+    return;
+  }
+  TM_CNT(kCtrVSkip, 1);
+  const int owner = path[L - 1];
+  const int os = __ldg(c.g.ptr[1] + owner), oe = __ldg(c.g.ptr[1] + owner + 1);
+  for (int i = lane; i < nu; i += 32) {
+    const int a = use[i];
+    if (a == owner || a == c.u || a == c.v) continue;
+    bool dup = false;
+#pragma unroll
+    for (int q = 0; q + 1 < L; ++q) dup |= (path[q] == a);
+    if (dup || !exists_pair(c, 1, owner, os, oe, a)) continue;
+    chain_pick<MAXD, L, true>(c, cg, t.row, t.grp, path, a, acc, next);
+  }
+}
+
+__device__ __forceinline__ void pull_dispatch(const Ctx &c, const CycGroup &cg, const Task &t, int lane,
+                                              CycAcc &acc, const Queue &next) {
+  switch (cg.maxd * 8 + (t.level & 7)) {
+#define TM_PULL_CASE(D_, L_) \
+  case D_ * 8 + L_: pull_task<D_, L_>(c, cg, t, lane, acc, next); return;
+    TM_PULL_CASE(2, 1)
+    TM_PULL_CASE(3, 1) TM_PULL_CASE(3, 2)
+    TM_PULL_CASE(4, 1) TM_PULL_CASE(4, 2) TM_PULL_CASE(4, 3)
+    TM_PULL_CASE(5, 1) TM_PULL_CASE(5, 2) TM_PULL_CASE(5, 3) TM_PULL_CASE(5, 4)
+#undef TM_PULL_CASE
+    default: return;
+  }
+}
+
 struct GlobalSink {  // contributions of one task item, straight to global memory
   long long *orow;
   int32_t *scr;  // scratch slot of the row (stack a, c, cycle_3 raw)
@@ -520,15 +707,19 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
       GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
       for (int j = t.a + lane; j < t.b; j += 32) {
         if (t.level == kLvlDomU) u_item(c, P, gr, j, sk);
-        else v_item(c, P, gr, t.grp, t.row, j, sk, next);
+        else v_item<true>(c, P, gr, t.grp, t.row, j, sk, next);
       }
     } else {  // chain task: resume the enumeration at level t.level
       CycAcc acc;
 #pragma unroll
       for (int k = 0; k < kMaxCyc; ++k) acc.e[k] = 0;
-      const int path[kMaxChain] = {t.path[0], t.path[1], t.path[2], t.path[3], t.path[4]};
-      for (int j = t.a + lane; j < t.b; j += 32)  // one entry per lane per step
-        cycles_resume(c, gr.cyc, t.row, t.grp, t.level, path, j, j + 1, acc, next);
+      if (t.level & kPullFlag) {
+        pull_dispatch(c, gr.cyc, t, lane, acc, next);
+      } else {
+        const int path[kMaxChain] = {t.path[0], t.path[1], t.path[2], t.path[3], t.path[4]};
+        for (int j = t.a + lane; j < t.b; j += 32)  // one entry per lane per step
+          cycles_resume(c, gr.cyc, t.row, t.grp, t.level, path, j, j + 1, acc, next);
+      }
 #pragma unroll
       for (int k = 0; k < kMaxCyc; ++k) {
         const long long s = warp_sum(acc.e[k]);
@@ -724,7 +915,7 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     }
     // task rounds: domain tasks, then one per chain level below a1
     if (dp.gr[k].udom || dp.gr[k].vdom)
-      rounds = std::max(rounds, 1 + std::max(0, dp.gr[k].cyc.maxd - 1));
+      rounds = std::max(rounds, 2 + std::max(0, dp.gr[k].cyc.maxd - 1));  // + 1: declined pull tasks
   }
 
   long long *d_out;
