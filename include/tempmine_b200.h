@@ -26,6 +26,10 @@
  *                        engine.py:455-513 (records; host dedup + sort)
  *   tm_csv_format /      FeatureMatrix.to_csv engine.py:73-103 (GPU int->text)
  *   tm_csv_fetch
+ *   tm_ingest_csv /      txgraph.parse_transactions txgraph.py:253-314 +
+ *   tm_ingest_fetch /    build_graph :317-354 (CSV rows -> dense first-seen
+ *   tm_ingest_vocab /    node ids, ticks, amounts, currency codes, labels)
+ *   tm_ingest_graph
  *   tm_last_error        Python exceptions EngineInvariantError /
  *                        ValueError (engine.py:33,589,669-670)
  *
@@ -45,7 +49,7 @@
 extern "C" {
 #endif
 
-#define TM_ABI_VERSION 3
+#define TM_ABI_VERSION 4
 
 /* pattern families (plan.py kernel hints + the extended north-star set) */
 enum tm_family {
@@ -265,6 +269,81 @@ int tm_vm_collect(tm_graph *g, const tm_vm_program *prog, int32_t plan_index, in
 
 /* Members attribution of triggers [lo, hi): host out[n_edges] (overwritten). */
 int tm_vm_members(tm_graph *g, const tm_vm_program *prog, int64_t lo, int64_t hi, int64_t *out);
+
+/* ------------------------------------------------------------------ ingestion
+ *
+ * tm_ingest_csv replaces txgraph.parse_transactions (txgraph.py:253-314) +
+ * build_graph (:317-354): the data rows of a delimited transaction log (the
+ * bytes AFTER the header row; the host resolves the header against the
+ * ColumnMapping, _resolve_columns :207-234) are split, parsed and given
+ * dense first-seen node ids and currency codes on the GPU.  Row semantics
+ * follow csv.reader (excel dialect, no quoted fields: a '"' anywhere is
+ * TM_PARSE_UNSUPPORTED) and the reference's per-row checks, in its order.
+ */
+enum tm_parse_status {
+  TM_PARSE_OK = 0,
+  TM_PARSE_COLUMNS = 1,      /* fewer than needed + 1 fields (:289-290) */
+  TM_PARSE_TIMESTAMP = 2,    /* not an int, and no / no matching strptime format (:237-247) */
+  TM_PARSE_NEGATIVE = 3,     /* negative timestamp (:294-295) */
+  TM_PARSE_AMOUNT = 4,       /* float() would fail (:296) */
+  TM_PARSE_LABEL = 5,        /* unrecognized label value (:307-308) */
+  TM_PARSE_UNSUPPORTED = 6,  /* valid for Python but outside the GPU parser */
+  TM_PARSE_COLLISION = 7     /* two distinct keys share a 64-bit hash (never expected) */
+};
+
+/* strptime program ops (ColumnMapping.timestamp_format, compiled host-side) */
+enum tm_fmt_op {
+  TM_FMT_END = 0, TM_FMT_LIT = 1, TM_FMT_SPACE = 2, TM_FMT_Y = 3, TM_FMT_y = 4, TM_FMT_m = 5,
+  TM_FMT_d = 6, TM_FMT_H = 7, TM_FMT_M = 8, TM_FMT_S = 9
+};
+#define TM_FMT_MAX 48
+
+typedef struct tm_csv_mapping {
+  /* field index per mapped column, -1 = not mapped (ColumnMapping fields) */
+  int32_t col_timestamp, col_src_bank, col_src_account, col_dst_bank, col_dst_account;
+  int32_t col_amount, col_currency, col_label;
+  int32_t needed;        /* max mapped index: rows need needed + 1 fields */
+  int32_t delimiter;     /* one byte */
+  int64_t tick_seconds;  /* >= 1; divides parsed datetimes only */
+  int32_t n_fmt;         /* 0: integer timestamps only (timestamp_format None) */
+  int32_t fmt_op[TM_FMT_MAX], fmt_arg[TM_FMT_MAX];
+} tm_csv_mapping;
+
+typedef struct tm_ingest_info {
+  int64_t n_rows;      /* data rows seen by csv.reader (blank rows included) */
+  int64_t n_edges;     /* records */
+  int64_t n_nodes;     /* distinct (bank, account) keys */
+  int64_t n_currency;  /* distinct currency strings */
+  int64_t err_row;     /* -1, or 0-based data row of the first failing row */
+  int32_t err_status;  /* enum tm_parse_status of that row */
+  int32_t pad;
+  int64_t err_begin, err_end;  /* byte span of that row in the input */
+} tm_ingest_info;
+
+typedef struct tm_ingest tm_ingest;
+
+/* Parse `len` bytes (host, or device when on_device) on `device`.  On a
+ * row error the call still succeeds (returns 0) with info->err_row >= 0 so
+ * the host can raise ParseError(line = err_row + 2) with the reference's
+ * message; *out is then NULL. */
+int tm_ingest_csv(int device, const char *buf, int64_t len, int on_device, const tm_csv_mapping *m,
+                  void *stream, tm_ingest **out, tm_ingest_info *info);
+
+/* Host copies of the edge table (any pointer may be NULL):
+ * src/dst/time int64[E], amount float64[E], currency int32[E], label int8[E]
+ * (-1 = no label column), like build_graph's arrays. */
+int tm_ingest_fetch(tm_ingest *h, int64_t *src, int64_t *dst, int64_t *time, double *amount,
+                    int32_t *currency, int8_t *label);
+
+/* Currency vocabulary in code (first-seen) order: offsets int64[n_currency+1]
+ * into bytes (capacity cap; returns the byte total needed via offsets). */
+int tm_ingest_vocab(tm_ingest *h, int64_t *offsets, char *bytes, int64_t cap);
+
+/* Build the device graph straight from the parsed device-resident edge
+ * arrays (no host round trip), as tm_graph_build with inputs_on_device. */
+int tm_ingest_graph(tm_ingest *h, tm_graph **out);
+
+void tm_ingest_free(tm_ingest *h);
 
 /* on = 1: bracket the mining kernels of every tm_mine with CUDA events on
  * the launch stream (read back by tm_last_mine_stats). */

@@ -72,6 +72,25 @@ class TmGraphInfo(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
+TM_FMT_MAX = 48
+
+
+class TmCsvMapping(ctypes.Structure):
+    _fields_ = [("col_timestamp", ctypes.c_int32), ("col_src_bank", ctypes.c_int32),
+                ("col_src_account", ctypes.c_int32), ("col_dst_bank", ctypes.c_int32),
+                ("col_dst_account", ctypes.c_int32), ("col_amount", ctypes.c_int32),
+                ("col_currency", ctypes.c_int32), ("col_label", ctypes.c_int32),
+                ("needed", ctypes.c_int32), ("delimiter", ctypes.c_int32),
+                ("tick_seconds", ctypes.c_int64), ("n_fmt", ctypes.c_int32),
+                ("fmt_op", ctypes.c_int32 * TM_FMT_MAX), ("fmt_arg", ctypes.c_int32 * TM_FMT_MAX)]
+
+
+class TmIngestInfo(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("n_edges", ctypes.c_int64), ("n_nodes", ctypes.c_int64),
+                ("n_currency", ctypes.c_int64), ("err_row", ctypes.c_int64), ("err_status", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("err_begin", ctypes.c_int64), ("err_end", ctypes.c_int64)]
+
+
 class TmMineStats(ctypes.Structure):
     _fields_ = [("triggers", ctypes.c_int64), ("heavy_triggers", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("light_ms", ctypes.c_float),
@@ -104,12 +123,18 @@ SIGNATURES = {
     "tm_vm_collect": (ctypes.c_int, [_P, ctypes.POINTER(TmVmProgram), ctypes.c_int32, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
     "tm_vm_members": (ctypes.c_int, [_P, ctypes.POINTER(TmVmProgram), ctypes.c_int64, ctypes.c_int64, _P]),
+    "tm_ingest_csv": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(TmCsvMapping),
+                                     _P, ctypes.POINTER(_P), ctypes.POINTER(TmIngestInfo)]),
+    "tm_ingest_fetch": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "tm_ingest_vocab": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64]),
+    "tm_ingest_graph": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "tm_ingest_free": (None, [_P]),
     "tm_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
     "tm_kernel_launch_count": (ctypes.c_int64, []),
     "tm_last_error": (ctypes.c_char_p, []),
     "tm_graph_free": (None, [_P]),
 }
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 class TempmineError(RuntimeError):

@@ -17,7 +17,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libtempmine_b200.so"
-SOURCES = ["tm_api.cu", "tm_sort.cu", "tm_graph.cu", "tm_mine.cu", "tm_members.cu", "tm_export.cu", "tm_instances.cu", "tm_vm.cu"]
+SOURCES = ["tm_api.cu", "tm_sort.cu", "tm_graph.cu", "tm_mine.cu", "tm_members.cu", "tm_export.cu", "tm_instances.cu", "tm_vm.cu", "tm_ingest.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -95,6 +95,27 @@ class DeviceGraph:
         self._attrs_on_device = True
 
     @classmethod
+    def _adopt(cls, handle: ctypes.c_void_p, node_count: int, edge_src, edge_dst, edge_time, edge_label,
+               edge_amount, edge_currency, currency_vocab, device: int) -> "DeviceGraph":
+        """Wrap a tm_graph built on the device (tm_ingest_graph): the host
+        keeps read-only copies of the edge table like any other DeviceGraph."""
+        self = cls.__new__(cls)
+        self.node_count = int(node_count)
+        self.edge_count = len(edge_src)
+        self.device = int(device)
+        self.edge_src, self.edge_dst, self.edge_time = edge_src, edge_dst, edge_time
+        self.edge_label = edge_label
+        self._h = handle
+        self._finalizer = weakref.finalize(self, _lib.load().tm_graph_free, handle)
+        self._stats = None
+        self._csr = {}
+        self.edge_amount = edge_amount
+        self.edge_currency = edge_currency
+        self.currency_vocab = tuple(currency_vocab) if currency_vocab is not None else None
+        self._attrs_on_device = False
+        return self
+
+    @classmethod
     def from_graph(cls, graph, device: int = 0) -> "DeviceGraph":
         return cls(graph.edge_src, graph.edge_dst, graph.edge_time, node_count=graph.node_count,
                    edge_label=getattr(graph, "edge_label", None), device=device,
