@@ -97,6 +97,12 @@ struct DevPlans {
   int32_t ngroups;
   DevPlan p[kMaxPlans];
   DevGroup gr[kMaxGroups];
+  // columns that receive item contributions (sg, gs, cycle_4..8) are staged
+  // in shared memory: slot[col] (-1: the owner lane writes it directly) and
+  // its inverse slot_col[slot]
+  int32_t n_stage;
+  int8_t slot[kMaxPlans];
+  int8_t slot_col[kMaxPlans];
 };
 
 // ----------------------------------------------------------------- errors

@@ -56,7 +56,10 @@ constexpr int kDomSplit = 256;       // a trigger slice above this becomes domai
 constexpr int kDeepSplit = 64;       // chain nodes with wider windows become chain tasks
 constexpr int kTaskSpan = 128;       // entries per task (4 per lane)
 constexpr int kLvlDomU = 8, kLvlDomV = 9;  // Task::level of domain tasks
-constexpr int kPullFlag = 32;  // Task::level bit: a whole wide window to expand backwards (pull_task)
+constexpr int kLvlPullV = 10;  // Task::level: gs + cycles of a hub v expanded from u's side
+// V-item parts (Task::pad0 of domain V tasks): stack's c, gs, cycles
+constexpr int kVStack = 1, kVGs = 2, kVCyc = 4, kVAll = 7;
+constexpr int kPullFlag = 32;  // Task::level bit: a whole wide window to expand backwards
 constexpr int kHostPieces = 4;     // host-output pieces overlapped with their D2H
 
 using namespace dev;
@@ -67,7 +70,7 @@ struct Task {
   int32_t row;   // trigger row (relative to lo); < 0 = empty slot
   int8_t grp;    // delta group
   int8_t level;  // 1..4: chain slice of a_level; kLvlDomU / kLvlDomV: trigger slice
-  int8_t pad0, pad1;
+  int8_t pad0, pad1;  // pad0: V-item parts of a domain V task (kV*)
   int32_t a, b;  // CSR range of the slice piece
   int32_t path[kMaxChain];  // chain a1..a_level; domain tasks: path[0] = scratch slot
 };
@@ -81,7 +84,7 @@ struct Queue {
 // cut [a, b) into kTaskSpan pieces; false (caller walks it itself) when the
 // queue is full — the walk is slower but exact and still on the GPU
 __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p1, int p2, int p3,
-                     int p4, int a, int b) {
+                     int p4, int a, int b, int parts = kVAll) {
   const int n = (b - a + kTaskSpan - 1) / kTaskSpan;
   TM_CNT(level >= kLvlDomU ? kCtrDomTask : kCtrChainTask, n);
   const int base = atomicAdd(qu.count, n);
@@ -94,7 +97,8 @@ __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p
     t.row = row;
     t.grp = (int8_t)grp;
     t.level = (int8_t)level;
-    t.pad0 = t.pad1 = 0;
+    t.pad0 = (int8_t)parts;
+    t.pad1 = 0;
     t.a = a + k * kTaskSpan;
     t.b = min(b, t.a + kTaskSpan);
     t.path[0] = p0; t.path[1] = p1; t.path[2] = p2; t.path[3] = p3; t.path[4] = p4;
@@ -208,70 +212,19 @@ __device__ __forceinline__ void close_at(const CycGroup &cg, int d, int cc, CycA
 // Chains a1..a_d of the cycle group (d <= MAXD):
 //   a1 in N+(v)\{u};  a_i in N+(a_{i-1}) \ {u, v, a1..a_{i-2}};
 //   cycle_{d+3} closes at depth d.
-// Level L walks entries j in [ja, jb) of the out-slice of a_L = path[L-1]
-// (L >= 1; level 0 is the V item loop) choosing a_{L+1}.  A chosen node
-// whose window exceeds kDeepSplit is expanded backwards (pull_level) when
-// the trigger's backward sets are small, else emitted as a chain task.
-template <int MAXD, int L, bool PI>
-__device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
-                                            int (&path)[kMaxChain], int ja, int jb, CycAcc &acc,
-                                            const Queue &qu);
-template <int MAXD, int J, bool PI>
-__device__ __forceinline__ bool pull_level(const Ctx &c, const CycGroup &cg, int row, int grp,
-                                           int (&path)[kMaxChain], const Win &ow, CycAcc &acc,
-                                           const Queue &qu);
-
-// a_{L+1} = a chosen (all exclusions checked): close at depth L + 1, descend.
-// PI: expand wide nodes backwards in place (task kernel); otherwise hand the
-// whole window to a pull task, keeping the warp kernel's walkers lean.
-template <int MAXD, int L, bool PI>
-__device__ __forceinline__ void chain_pick(const Ctx &c, const CycGroup &cg, int row, int grp,
-                                           int (&path)[kMaxChain], int a, CycAcc &acc,
-                                           const Queue &qu) {
-  TM_CNT(kCtrChain1 + L, 1);
-  const Win w = window(c, 1, a);  // a's out-window: closes and descends
-  if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, w, path), acc);
-  if constexpr (L + 1 < MAXD) {
-    path[L] = a;
-    if (w.len() > kDeepSplit) {
-      if constexpr (PI) {
-        if (pull_level<MAXD, L + 2, PI>(c, cg, row, grp, path, w, acc, qu)) return;
-        if (emit(qu, row, grp, L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b)) return;
-      } else {
-        if (emit_whole(qu, row, grp, (L + 1) | kPullFlag, path, w.a, w.b)) return;
-      }
-    }
-    chain_level<MAXD, L + 1, PI>(c, cg, row, grp, path, w.a, w.b, acc, qu);
-  }
-}
-
-template <int MAXD, int L, bool PI>
-__device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
-                                            int (&path)[kMaxChain], int ja, int jb, CycAcc &acc,
-                                            const Queue &qu) {
-  const int owner = path[L - 1];
-  for (int j = ja; j < jb; ++j) {
-    const int a = __ldg(c.g.nbr[1] + j);
-    if (a == owner || a == c.u || a == c.v) continue;
-    bool dup = false;
-#pragma unroll
-    for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
-    if (dup || !first_in_window(c, 1, j)) continue;
-    chain_pick<MAXD, L, PI>(c, cg, row, grp, path, a, acc, qu);
-  }
-}
-
-// Backward expansion for a wide chain node (a sender hub).  Every chain
-// that contributes reaches u through the window: a node at depth j closing
-// at depth d >= j lies in B_{2+d-j}, where B_1 = N-(u) \ {u, v} and
-// B_{k+1} = N-(B_k) \ {u, v} (windowed, distinct).  These sets are
-// supersets of the useful choices — pruning with them skips only chains
-// that add nothing — and they are small when in-degrees are, so the hub's
-// window is not walked: each useful node b is probed for owner -> b in the
-// pair index and, if present, picked exactly as the walk would pick it.
-// Declines (returns false) when a set overflows or is not much smaller than
-// the window; the caller then walks or emits tasks as before.
+// Level L chooses a_{L+1} among the out-neighbours of a_L = path[L-1]
+// (L >= 1; level 0 is the V item loop): either the window entries [ja, jb)
+// of a_L's out-run, or — for a wide a_L (a sender hub) — the candidate list
+// `cand[ja..jb)` of useful nodes (see useful_nodes), each probed for
+// a_L -> a.  Every level has ONE call site of the next, so the inlined
+// template tree stays linear in the depth.
 constexpr int kBCap = 48;
+
+// Backward sets: every chain that contributes reaches u inside the window,
+// so a node at depth j closing at depth d >= j lies in B_{2+d-j}, where
+// B_1 = N-(u) \ {u, v} and B_{k+1} = N-(B_k) \ {u, v} (windowed, distinct).
+// They are supersets of the useful choices — pruning with them skips only
+// chains that add nothing — and small when in-degrees are.
 __device__ __forceinline__ bool bset_add(int *node, int from, int &n, int m) {
   for (int i = from; i < n; ++i)
     if (node[i] == m) return true;
@@ -318,27 +271,70 @@ __device__ __noinline__ int useful_nodes(const DevGraph &g, int u, int v, uint32
   return nu;
 }
 
-template <int MAXD, int J, bool PI>
-__device__ __forceinline__ bool pull_level(const Ctx &c, const CycGroup &cg, int row, int grp,
-                                           int (&path)[kMaxChain], const Win &ow, CycAcc &acc,
-                                           const Queue &qu) {
-  static_assert(J >= 2 && J <= MAXD, "pull_level depth");
-  int use[kBCap];
-  const int nu = useful_nodes(c.g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, MAXD, J, use);
-  if (nu < 0 || nu * 4 > ow.len()) return false;
+// candidates for depth J under a wide window w of path[J-2]: true and
+// (ja, jb, cand) set when the backward sets are much smaller than w
+__device__ __forceinline__ bool pull_candidates(const Ctx &c, const CycGroup &cg, int maxd, int J,
+                                                const Win &w, int *use, int &ja, int &jb) {
+  const int nu = useful_nodes(c.g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, maxd, J, use);
+  if (nu < 0 || nu * 4 > w.len()) return false;
   TM_CNT(kCtrVSkip, 1);
-  const int owner = path[J - 2];
-  const int os = __ldg(c.g.ptr[1] + owner), oe = __ldg(c.g.ptr[1] + owner + 1);
-  for (int i = 0; i < nu; ++i) {
-    const int a = use[i];
+  ja = 0;
+  jb = nu;
+  return true;
+}
+
+template <int MAXD, int L, bool PI>
+__device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                            int (&path)[kMaxChain], int ja, int jb, const int *cand,
+                                            CycAcc &acc, const Queue &qu);
+
+// a_{L+1} = a chosen (all exclusions checked): close at depth L + 1, descend.
+// A wide a: PI (task kernel) expands it backwards in place, or splits it
+// into chain tasks; the warp kernel hands the whole window to a pull task,
+// keeping its walkers lean.
+template <int MAXD, int L, bool PI>
+__device__ __forceinline__ void chain_pick(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                           int (&path)[kMaxChain], int a, CycAcc &acc,
+                                           const Queue &qu) {
+  TM_CNT(kCtrChain1 + L, 1);
+  const Win w = window(c, 1, a);  // a's out-window: closes and descends
+  if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, w, path), acc);
+  if constexpr (L + 1 < MAXD) {
+    path[L] = a;
+    int ja = w.a, jb = w.b;
+    const int *cand = nullptr;
+    int use[kBCap];
+    if (w.len() > kDeepSplit) {
+      if constexpr (PI) {
+        if (pull_candidates(c, cg, MAXD, L + 2, w, use, ja, jb)) cand = use;
+        else if (emit(qu, row, grp, L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b)) return;
+      } else {
+        if (emit_whole(qu, row, grp, (L + 1) | kPullFlag, path, w.a, w.b)) return;
+      }
+    }
+    chain_level<MAXD, L + 1, PI>(c, cg, row, grp, path, ja, jb, cand, acc, qu);
+  }
+}
+
+template <int MAXD, int L, bool PI>
+__device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
+                                            int (&path)[kMaxChain], int ja, int jb, const int *cand,
+                                            CycAcc &acc, const Queue &qu) {
+  const int owner = path[L - 1];
+  int os = 0, oe = 0;
+  if (cand) {
+    os = __ldg(c.g.ptr[1] + owner);
+    oe = __ldg(c.g.ptr[1] + owner + 1);
+  }
+  for (int j = ja; j < jb; ++j) {
+    const int a = cand ? cand[j] : __ldg(c.g.nbr[1] + j);
     if (a == owner || a == c.u || a == c.v) continue;
     bool dup = false;
 #pragma unroll
-    for (int q = 0; q + 2 < J; ++q) dup |= (path[q] == a);
-    if (dup || !exists_pair(c, 1, owner, os, oe, a)) continue;
-    chain_pick<MAXD, J - 1, PI>(c, cg, row, grp, path, a, acc, qu);
+    for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
+    if (dup || !(cand ? exists_pair(c, 1, owner, os, oe, a) : first_in_window(c, 1, j))) continue;
+    chain_pick<MAXD, L, PI>(c, cg, row, grp, path, a, acc, qu);
   }
-  return true;
 }
 
 // cycles through chain node a1 = m (a V item), depths 1..maxd
@@ -346,15 +342,18 @@ template <int MAXD, bool PI>
 __device__ __forceinline__ void cycles_a1(const Ctx &c, const CycGroup &cg, int row, int grp,
                                           int (&path)[kMaxChain], const Win &w, CycAcc &acc,
                                           const Queue &qu) {
+  int ja = w.a, jb = w.b;
+  const int *cand = nullptr;
+  int use[kBCap];
   if (w.len() > kDeepSplit) {
     if constexpr (PI) {
-      if (pull_level<MAXD, 2, PI>(c, cg, row, grp, path, w, acc, qu)) return;
-      if (emit(qu, row, grp, 1, path[0], -1, -1, -1, -1, w.a, w.b)) return;
+      if (pull_candidates(c, cg, MAXD, 2, w, use, ja, jb)) cand = use;
+      else if (emit(qu, row, grp, 1, path[0], -1, -1, -1, -1, w.a, w.b)) return;
     } else {
       if (emit_whole(qu, row, grp, 1 | kPullFlag, path, w.a, w.b)) return;
     }
   }
-  chain_level<MAXD, 1, PI>(c, cg, row, grp, path, w.a, w.b, acc, qu);
+  chain_level<MAXD, 1, PI>(c, cg, row, grp, path, ja, jb, cand, acc, qu);
 }
 
 template <bool PI>
@@ -372,14 +371,15 @@ __device__ __forceinline__ void cycles_from_a1(const Ctx &c, const CycGroup &cg,
   }
 }
 
-// a chain task resumes at level L with a1..a_L given
+// a chain task resumes at level L with a1..a_L given (entries [ja, jb) of
+// a_L's window, or of a candidate list)
 __device__ __forceinline__ void cycles_resume(const Ctx &c, const CycGroup &cg, int row, int grp,
                                               int L, const int (&p0)[kMaxChain], int ja, int jb,
-                                              CycAcc &acc, const Queue &qu) {
+                                              const int *cand, CycAcc &acc, const Queue &qu) {
   int path[kMaxChain] = {p0[0], p0[1], p0[2], p0[3], p0[4]};
   switch (cg.maxd * 8 + L) {
 #define TM_CHAIN_CASE(D_, L_) \
-  case D_ * 8 + L_: chain_level<D_, L_, true>(c, cg, row, grp, path, ja, jb, acc, qu); return;
+  case D_ * 8 + L_: chain_level<D_, L_, true>(c, cg, row, grp, path, ja, jb, cand, acc, qu); return;
     TM_CHAIN_CASE(2, 1)
     TM_CHAIN_CASE(3, 1) TM_CHAIN_CASE(3, 2)
     TM_CHAIN_CASE(4, 1) TM_CHAIN_CASE(4, 2) TM_CHAIN_CASE(4, 3)
@@ -409,19 +409,17 @@ __device__ __forceinline__ void u_item(const Ctx &c, const DevPlans &P, const De
   }
 }
 
+// V item m (a distinct node of N+(v) \ {u, v}); parts: kV* bits
 template <bool PI, class Sink>
-__device__ __forceinline__ void v_item(const Ctx &c, const DevPlans &P, const DevGroup &gr, int grp,
-                                       int row, int j, Sink &sk, const Queue &qu) {
-  const int m = __ldg(c.g.nbr[1] + j);
-  TM_CNT(kCtrVWalk, 1);
-  if (m == c.u || m == c.v || !first_in_window(c, 1, j)) return;
+__device__ __forceinline__ void v_node(const Ctx &c, const DevPlans &P, const DevGroup &gr, int grp,
+                                       int row, int m, Sink &sk, const Queue &qu, int parts) {
   TM_CNT(kCtrVItem, 1);
-  if (gr.has_stack) sk.sc();
-  for (int i = 0; i < gr.n_gs; ++i) {  // gs: destination m (Appendix B)
+  if (gr.has_stack && (parts & kVStack)) sk.sc();
+  for (int i = 0; i < gr.n_gs && (parts & kVGs); ++i) {  // gs: destination m (Appendix B)
     const int ci = gr.gs_col[i], K = P.p[ci].min_size;
     if (inner_hits(c, m, 0, c.u, 1, c.wuo, K, c.u != c.v ? c.v : -1) >= K) sk.col(ci, 1);
   }
-  if (gr.cyc.maxd >= 1 && c.u != c.v && c.wui.len() > 0) {
+  if ((parts & kVCyc) && gr.cyc.maxd >= 1 && c.u != c.v && c.wui.len() > 0) {
     CycAcc acc;
 #pragma unroll
     for (int e = 0; e < kMaxCyc; ++e) acc.e[e] = 0;
@@ -456,15 +454,18 @@ struct WarpShared {
   uint32_t lo[32], hi[32];
   Win wui[32], wuo[32], wvi[32], wvo[32];
   int excl[32];
-  int sa[32], sc[32], c3[32];
+  int sa[32], sc[32];
+  int c3[32];  // cycle_3 raw count (low bits) | V-item parts the warp walks << kPartsShift
 };
+constexpr int kPartsShift = 28;  // c3 counts stay far below 2^28 (an in-window degree)
 
 struct SmemSink {  // contributions of row `owner` into the warp's shared state
   WarpShared &ws;
-  long long *stage;
-  int owner, C;
+  long long *stage;  // [32][S] staged columns
+  const int8_t *slot;
+  int owner, S;
   __device__ __forceinline__ void col(int ci, long long v) {
-    atomicAdd(reinterpret_cast<unsigned long long *>(stage + owner * C + ci), (unsigned long long)v);
+    atomicAdd(reinterpret_cast<unsigned long long *>(stage + owner * S + slot[ci]), (unsigned long long)v);
   }
   __device__ __forceinline__ void sa() { atomicAdd(&ws.sa[owner], 1); }
   __device__ __forceinline__ void sc() { atomicAdd(&ws.sc[owner], 1); }
@@ -515,12 +516,13 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     int64_t n_rows, long long *__restrict__ out, Queue qu, int32_t *__restrict__ split_rows,
     int32_t *__restrict__ split_n, int32_t *__restrict__ scratch, int32_t split_cap,
     const int32_t *__restrict__ order) {
-  extern __shared__ long long stage_all[];  // [warp][32][C]
+  extern __shared__ long long stage_all[];  // [warp][32][S]: the staged (item) columns only —
+                                            // shared memory left unused is L1 for the walkers
   __shared__ WarpShared wsh[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpShared &ws = wsh[warp];
-  const int C = P.n;
-  long long *stage = stage_all + (size_t)warp * 32 * C;
+  const int C = P.n, S = P.n_stage;
+  long long *stage = stage_all + (size_t)warp * 32 * S;
   const int64_t wrow0 = (int64_t)blockIdx.x * kThreads + warp * 32;
   const int64_t pos = wrow0 + lane;  // position in processing order
   const bool valid = pos < n_rows;
@@ -536,8 +538,9 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     v = __ldg(g.e_dst + e);
     r = __ldg(g.e_rank + e);
   }
-  for (int i = 0; i < C; ++i) stage[lane * C + i] = 0;
+  for (int i = 0; i < S; ++i) stage[lane * S + i] = 0;
   if (valid) TM_CNT(kCtrTrig, 1);
+  long long *orow = out + row * C;  // the lane's own row (valid lanes only)
 
   for (int gi = 0; gi < P.ngroups; ++gi) {
     const DevGroup &gr = P.gr[gi];
@@ -554,17 +557,18 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
           long long n = w.len() - loops_in_window(c, x);
           if (p.exclude_trigger && u != v) n -= 1;
           if (p.min_size > 1 && n < p.min_size) n = 0;
-          stage[lane * C + ci] = n;
+          orow[ci] = n;
         } else if (p.family == TM_CYCLE && p.cycle_len == 2) {
           const long long raw = (u != v && exists_in(c, 1, v, c.wvo, u)) ? 1 : 0;
-          stage[lane * C + ci] = raw >= p.min_size ? raw : 0;
+          orow[ci] = raw >= p.min_size ? raw : 0;
         }
       }
     }
     if (!gr.udom && !gr.vdom) continue;
     ws.u[lane] = u; ws.v[lane] = v; ws.lo[lane] = c.lo; ws.hi[lane] = c.hi;
     ws.wui[lane] = c.wui; ws.wuo[lane] = c.wuo; ws.wvi[lane] = c.wvi; ws.wvo[lane] = c.wvo;
-    ws.sa[lane] = ws.sc[lane] = ws.c3[lane] = 0;
+    ws.sa[lane] = ws.sc[lane] = 0;
+    int vparts = kVAll;
     // slices too long for the warp become domain tasks
     int ulen = (valid && gr.udom) ? c.wui.len() : 0;
     int vlen = (valid && gr.vdom) ? c.wvo.len() : 0;
@@ -582,24 +586,41 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
       if (slot != -2) {
         if (ulen > kDomSplit && emit(qu, (int)row, gi, kLvlDomU, slot, -1, -1, -1, -1, c.wui.a, c.wui.b))
           ulen = 0;
-        if (vlen > kDomSplit && emit(qu, (int)row, gi, kLvlDomV, slot, -1, -1, -1, -1, c.wvo.a, c.wvo.b))
-          vlen = 0;
+        if (vlen > kDomSplit) {
+          // a hub v: gs and cycles go to one pull task (expanded from u's
+          // side, which is small); stack's c is a cheap distinct count the
+          // domain tasks stream.  Any emission that fails is walked here.
+          const bool pullable = gr.n_gs > 0 || gr.cyc.maxd >= 1;
+          int parts = kVAll;
+          if (pullable) {
+            const int path[kMaxChain] = {slot, -1, -1, -1, -1};
+            if (emit_whole(qu, (int)row, gi, kLvlPullV, path, c.wvo.a, c.wvo.b)) parts = gr.has_stack ? kVStack : 0;
+          }
+          if (parts && emit(qu, (int)row, gi, kLvlDomV, slot, -1, -1, -1, -1, c.wvo.a, c.wvo.b, parts)) parts = 0;
+          if (!parts) vlen = 0;
+          vparts = parts;
+        }
       }
     }
+    ws.c3[lane] = vparts << kPartsShift;
     __syncwarp();
     flat_for(ws, lane, ulen, [&](int o, int k) {
       const Ctx co = ctx_of(g, ws, o);
-      SmemSink sk{ws, stage, o, C};
+      SmemSink sk{ws, stage, P.slot, o, S};
       u_item(co, P, gr, co.wui.a + k, sk);
     });
     flat_for(ws, lane, vlen, [&](int o, int k) {
       const Ctx co = ctx_of(g, ws, o);
-      SmemSink sk{ws, stage, o, C};
-      v_item<false>(co, P, gr, gi, ws.rowid[o], co.wvo.a + k, sk, qu);
+      SmemSink sk{ws, stage, P.slot, o, S};
+      const int j = co.wvo.a + k;
+      const int m = __ldg(g.nbr[1] + j);
+      TM_CNT(kCtrVWalk, 1);
+      if (m == co.u || m == co.v || !first_in_window(co, 1, j)) return;
+      v_node<false>(co, P, gr, gi, ws.rowid[o], m, sk, qu, ws.c3[o] >> kPartsShift);
     });
     // whole-count columns: stack a * c (kernels.py:379-402), cycle_3 threshold
     if (valid) {
-      const long long a = ws.sa[lane], d = ws.sc[lane], c3 = ws.c3[lane];
+      const long long a = ws.sa[lane], d = ws.sc[lane], c3 = ws.c3[lane] & ((1 << kPartsShift) - 1);
       if (slot >= 0) {
         scratch[3 * slot] = (int)a;
         scratch[3 * slot + 1] = (int)d;
@@ -609,9 +630,9 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
         const int ci = gr.cols[i];
         const DevPlan &p = P.p[ci];
         if (p.family == TM_STACK)
-          stage[lane * C + ci] = (a > 0 && d > 0 && a >= p.min_size && d >= p.min_size) ? a * d : 0;
+          orow[ci] = (a > 0 && d > 0 && a >= p.min_size && d >= p.min_size) ? a * d : 0;
         else if (p.family == TM_CYCLE && p.cycle_len == 3)
-          stage[lane * C + ci] = c3 >= p.min_size ? c3 : 0;
+          orow[ci] = c3 >= p.min_size ? c3 : 0;
       }
     }
     __syncwarp();
@@ -619,63 +640,16 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
   __syncwarp();
   if (order) {  // permuted rows: each lane writes its own
     if (valid)
-      for (int i = 0; i < C; ++i) out[row * C + i] = stage[lane * C + i];
+      for (int i = 0; i < S; ++i) orow[P.slot_col[i]] = stage[lane * S + i];
     return;
   }
   const int64_t left = n_rows - wrow0;
   const int nrow = left < 32 ? (int)(left > 0 ? left : 0) : 32;
   long long *dst = out + wrow0 * C;
-  for (int i = lane; i < nrow * C; i += 32) dst[i] = stage[i];
+  for (int i = lane; i < nrow * S; i += 32) dst[(i / S) * C + P.slot_col[i % S]] = stage[i];
 }
 
 // ------------------------------------------------------------ tasks
-
-// a pull task: owner a_L = path[L-1] with the whole wide window [t.a, t.b);
-// the warp expands it backwards (every lane builds the same sets — uniform
-// loads — then the lanes share the useful nodes), or, when the sets decline,
-// splits it into chain tasks for the next round (walks it when that queue is
-// full).
-template <int MAXD, int L>
-__device__ __forceinline__ void pull_task(const Ctx &c, const CycGroup &cg, const Task &t, int lane,
-                                          CycAcc &acc, const Queue &next) {
-  int path[kMaxChain] = {t.path[0], t.path[1], t.path[2], t.path[3], t.path[4]};
-  int use[kBCap];
-  const int nu = useful_nodes(c.g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, MAXD, L + 1, use);
-  if (nu < 0 || nu * 4 > t.b - t.a) {
-    bool ok = false;
-    if (lane == 0) ok = emit(next, t.row, t.grp, L, path[0], path[1], path[2], path[3], path[4], t.a, t.b);
-    if (__shfl_sync(0xffffffffu, ok, 0)) return;
-    for (int j = t.a + lane; j < t.b; j += 32)
-      chain_level<MAXD, L, true>(c, cg, t.row, t.grp, path, j, j + 1, acc, next);
-    return;
-  }
-  TM_CNT(kCtrVSkip, 1);
-  const int owner = path[L - 1];
-  const int os = __ldg(c.g.ptr[1] + owner), oe = __ldg(c.g.ptr[1] + owner + 1);
-  for (int i = lane; i < nu; i += 32) {
-    const int a = use[i];
-    if (a == owner || a == c.u || a == c.v) continue;
-    bool dup = false;
-#pragma unroll
-    for (int q = 0; q + 1 < L; ++q) dup |= (path[q] == a);
-    if (dup || !exists_pair(c, 1, owner, os, oe, a)) continue;
-    chain_pick<MAXD, L, true>(c, cg, t.row, t.grp, path, a, acc, next);
-  }
-}
-
-__device__ __forceinline__ void pull_dispatch(const Ctx &c, const CycGroup &cg, const Task &t, int lane,
-                                              CycAcc &acc, const Queue &next) {
-  switch (cg.maxd * 8 + (t.level & 7)) {
-#define TM_PULL_CASE(D_, L_) \
-  case D_ * 8 + L_: pull_task<D_, L_>(c, cg, t, lane, acc, next); return;
-    TM_PULL_CASE(2, 1)
-    TM_PULL_CASE(3, 1) TM_PULL_CASE(3, 2)
-    TM_PULL_CASE(4, 1) TM_PULL_CASE(4, 2) TM_PULL_CASE(4, 3)
-    TM_PULL_CASE(5, 1) TM_PULL_CASE(5, 2) TM_PULL_CASE(5, 3) TM_PULL_CASE(5, 4)
-#undef TM_PULL_CASE
-    default: return;
-  }
-}
 
 struct GlobalSink {  // contributions of one task item, straight to global memory
   long long *orow;
@@ -688,6 +662,64 @@ struct GlobalSink {  // contributions of one task item, straight to global memor
   __device__ __forceinline__ void c3() { atomicAdd(scr + 2, 1); }
 };
 
+// gs of a trigger whose v is a hub, from u's side: with threshold K >= 2, d
+// counts when 1 (v itself) + #{n in N+(u) \ {u, v, d} : n -> d} >= K, so
+// the candidates are the 2-hop out-neighbourhood of u, enumerated (lane 0)
+// when small and each probed for v -> d.  False: declined (walk instead).
+__device__ __forceinline__ bool pull_gs(const Ctx &c, const DevPlans &P, const DevGroup &gr, int vs, int ve,
+                                        int lane, long long *orow) {
+  bool ok = c.u != c.v && c.wuo.len() <= 32;
+  for (int i = 0; i < gr.n_gs; ++i) ok &= P.p[gr.gs_col[i]].min_size >= 2;
+  constexpr int kPairs = 128;
+  if (ok && lane == 0) {
+    int pd[kPairs], np = 0;
+    for (int j = c.wuo.a; j < c.wuo.b && ok; ++j) {
+      const int n = __ldg(c.g.nbr[1] + j);
+      if (n == c.u || n == c.v || !first_in_window(c, 1, j)) continue;
+      const Win w = window(c, 1, n);
+      if (np + w.len() > kPairs) {
+        ok = false;
+        break;
+      }
+      for (int k = w.a; k < w.b; ++k) {
+        const int d = __ldg(c.g.nbr[1] + k);
+        if (d == c.u || d == c.v || d == n || !first_in_window(c, 1, k)) continue;
+        pd[np++] = d;
+      }
+    }
+    if (ok) {
+      long long cnt[kMaxPlans] = {};
+      for (int i = 0; i < np; ++i) {
+        bool seen = false;
+        for (int q = 0; q < i && !seen; ++q) seen = pd[q] == pd[i];
+        if (seen) continue;
+        int hits = 2;  // v, and the n of this first occurrence
+        for (int q = i + 1; q < np; ++q) hits += pd[q] == pd[i];
+        bool member = false, probed = false;
+        for (int gi = 0; gi < gr.n_gs; ++gi) {
+          if (hits < P.p[gr.gs_col[gi]].min_size) continue;
+          if (!probed) member = exists_pair(c, 1, c.v, vs, ve, pd[i]), probed = true;
+          if (member) ++cnt[gi];
+        }
+      }
+      for (int gi = 0; gi < gr.n_gs; ++gi)
+        if (cnt[gi])
+          atomicAdd(reinterpret_cast<unsigned long long *>(orow + gr.gs_col[gi]), (unsigned long long)cnt[gi]);
+    }
+  }
+  return __shfl_sync(0xffffffffu, ok, 0);
+}
+
+// Task kinds (one warp per task):
+//   kLvlDomU / kLvlDomV   a piece of a trigger's U / V slice, lane per entry
+//   kLvlPullV             a hub v's whole N+(v): gs from u's side (pull_gs),
+//                         cycles through the useful a1 only (the depth-1
+//                         backward sets), each probed for v -> a1 — declined
+//                         parts go back to the queue as domain V tasks
+//   level | kPullFlag     a wide chain node's whole window: its useful
+//                         nodes, or chain tasks for the next round
+//   level 1..4            a piece of a chain node's window
+// Each kind feeds ONE call site of the item / chain code below.
 __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next) {
@@ -703,28 +735,84 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     Ctx c{g, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {}};
     trigger_windows(c, gr, t.row);
     long long *orow = out + (int64_t)t.row * P.n;
-    if (t.level == kLvlDomU || t.level == kLvlDomV) {
+    int use[kBCap];
+    if (t.level == kLvlDomU) {
       GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
-      for (int j = t.a + lane; j < t.b; j += 32) {
-        if (t.level == kLvlDomU) u_item(c, P, gr, j, sk);
-        else v_item<true>(c, P, gr, t.grp, t.row, j, sk, next);
+      for (int j = t.a + lane; j < t.b; j += 32) u_item(c, P, gr, j, sk);
+    } else if (t.level == kLvlDomV || t.level == kLvlPullV) {
+      GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
+      int parts = t.pad0, ja = t.a, jb = t.b;
+      const int *cand = nullptr;
+      const int vs = __ldg(g.ptr[1] + c.v), ve = __ldg(g.ptr[1] + c.v + 1);
+      if (t.level == kLvlPullV) {
+        int redo = 0;
+        parts = 0;
+        if (gr.n_gs > 0 && !pull_gs(c, P, gr, vs, ve, lane, orow)) redo |= kVGs;
+        const CycGroup &cg = gr.cyc;
+        if (cg.maxd >= 1 && c.u != c.v && c.wui.len() > 0) {
+          const int nu = useful_nodes(g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, cg.maxd, 1, use);
+          if (nu < 0 || nu * 4 > t.b - t.a) {
+            redo |= kVCyc;
+          } else {
+            cand = use;
+            ja = 0;
+            jb = nu;
+            parts = kVCyc;
+          }
+        }
+        if (redo) {
+          bool ok = false;
+          if (lane == 0) ok = emit(next, t.row, t.grp, kLvlDomV, t.path[0], -1, -1, -1, -1, t.a, t.b, redo);
+          if (!__shfl_sync(0xffffffffu, ok, 0)) {  // queue full: this warp walks the declined parts too
+            if (cand) {
+              for (int j = t.a + lane; j < t.b; j += 32) {
+                const int m = __ldg(g.nbr[1] + j);
+                if (m == c.u || m == c.v || !first_in_window(c, 1, j)) continue;
+                if (redo & kVGs) v_node<true>(c, P, gr, t.grp, t.row, m, sk, next, kVGs);
+              }
+            } else {
+              parts = redo;
+            }
+          }
+        }
+        if (!parts) ja = jb = 0;
       }
-    } else {  // chain task: resume the enumeration at level t.level
+      for (int k = ja + lane; k < jb; k += 32) {
+        int m;
+        if (cand) {
+          m = cand[k];
+          if (m == c.u || m == c.v || !exists_pair(c, 1, c.v, vs, ve, m)) continue;
+        } else {
+          m = __ldg(g.nbr[1] + k);
+          if (m == c.u || m == c.v || !first_in_window(c, 1, k)) continue;
+        }
+        v_node<true>(c, P, gr, t.grp, t.row, m, sk, next, parts);
+      }
+    } else {  // a chain node's window (or its useful nodes)
       CycAcc acc;
 #pragma unroll
       for (int k = 0; k < kMaxCyc; ++k) acc.e[k] = 0;
+      const int L = t.level & 7;
+      const int path[kMaxChain] = {t.path[0], t.path[1], t.path[2], t.path[3], t.path[4]};
+      int ja = t.a, jb = t.b;
+      const int *cand = nullptr;
       if (t.level & kPullFlag) {
-        pull_dispatch(c, gr.cyc, t, lane, acc, next);
-      } else {
-        const int path[kMaxChain] = {t.path[0], t.path[1], t.path[2], t.path[3], t.path[4]};
-        for (int j = t.a + lane; j < t.b; j += 32)  // one entry per lane per step
-          cycles_resume(c, gr.cyc, t.row, t.grp, t.level, path, j, j + 1, acc, next);
+        const Win w{t.a, t.b};
+        if (pull_candidates(c, gr.cyc, gr.cyc.maxd, L + 1, w, use, ja, jb)) {
+          cand = use;
+        } else {
+          bool ok = false;
+          if (lane == 0) ok = emit(next, t.row, t.grp, L, path[0], path[1], path[2], path[3], path[4], t.a, t.b);
+          if (__shfl_sync(0xffffffffu, ok, 0)) ja = jb = 0;  // split into chain tasks for the next round
+        }
       }
+      for (int k = ja + lane; k < jb; k += 32)  // one entry per lane per step
+        cycles_resume(c, gr.cyc, t.row, t.grp, L, path, k, k + 1, cand, acc, next);
 #pragma unroll
       for (int k = 0; k < kMaxCyc; ++k) {
-        const long long s = warp_sum(acc.e[k]);
-        if (lane == 0 && k < gr.cyc.n && s)
-          atomicAdd(reinterpret_cast<unsigned long long *>(orow + gr.cyc.col[k]), (unsigned long long)s);
+        const long long sum = warp_sum(acc.e[k]);
+        if (lane == 0 && k < gr.cyc.n && sum)
+          atomicAdd(reinterpret_cast<unsigned long long *>(orow + gr.cyc.col[k]), (unsigned long long)sum);
       }
     }
   }
@@ -915,7 +1003,7 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     }
     // task rounds: domain tasks, then one per chain level below a1
     if (dp.gr[k].udom || dp.gr[k].vdom)
-      rounds = std::max(rounds, 2 + std::max(0, dp.gr[k].cyc.maxd - 1));  // + 1: declined pull tasks
+      rounds = std::max(rounds, 3 + std::max(0, dp.gr[k].cyc.maxd - 1));  // + 2: declined pull tasks
   }
 
   long long *d_out;
@@ -937,7 +1025,13 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   Queue qa{g->tasks.as<Task>(), cnt + 1, (int32_t)task_cap};
   Queue qb{g->tasks.as<Task>() + task_cap, cnt + 2, (int32_t)task_cap};
 
-  const size_t smem = sizeof(long long) * kThreads * n_plans;
+  for (int i = 0; i < n_plans; ++i) {
+    const int f = plans[i].family;
+    const bool staged = f == TM_SG || f == TM_GS || (f == TM_CYCLE && plans[i].cycle_len >= 4);
+    dp.slot[i] = (int8_t)(staged ? dp.n_stage : -1);
+    if (staged) dp.slot_col[dp.n_stage++] = (int8_t)i;
+  }
+  const size_t smem = sizeof(long long) * kThreads * std::max(dp.n_stage, 1);
   if (smem > 48 * 1024)
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // Host output: mine the range in pieces and copy each finished piece back
