@@ -170,6 +170,26 @@ int DevBuf::ensure_on(size_t n, cudaStream_t s) {
   return TM_OK;
 }
 
+int DevBuf::ensure_pooled(size_t n, cudaStream_t s) {
+  if (n <= bytes && p) return TM_OK;
+  if (p) {
+    cudaDeviceSynchronize();  // earlier calls on other streams may still use the old block
+    release();
+  }
+  cudaError_t e = cudaMallocAsync(&p, n ? n : 16, s);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? TM_E_OOM : TM_E_CUDA,
+                std::string("device allocation of ") + std::to_string(n) +
+                    " bytes failed: " + cudaGetErrorString(e));
+  }
+  bytes = n ? n : 16;
+  pooled = true;
+  pool_stream = nullptr;
+  return TM_OK;
+}
+
 int DevBuf::ensure(size_t n) {
   if (n <= bytes && p) return TM_OK;
   release();
@@ -475,8 +495,8 @@ extern "C" void tm_graph_free(tm_graph *g) {
   cudaStream_t s = g->stream;
   for (int i = 0; i < 3; ++i)
     if (g->ev[i]) cudaEventDestroy(g->ev[i]);
-  for (int i = 0; i < 4; ++i)
-    if (g->piece_ev[i]) cudaEventDestroy(g->piece_ev[i]);
+  for (cudaEvent_t e : g->piece_ev)
+    if (e) cudaEventDestroy(e);
   if (g->copy_stream) {
     cudaStreamSynchronize(g->copy_stream);
     cudaStreamDestroy(g->copy_stream);

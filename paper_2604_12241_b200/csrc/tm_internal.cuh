@@ -137,8 +137,8 @@ struct DevBuf {
   ~DevBuf() { release(); }
   void release() {
     if (p) {
-      if (pooled) cudaFreeAsync(p, pool_stream);
-      else cudaFree(p);
+      if (pooled && pool_stream) cudaFreeAsync(p, pool_stream);
+      else cudaFree(p);  // also valid for pool memory: frees synchronously, back into the pool
     }
     p = nullptr;
     bytes = 0;
@@ -146,6 +146,10 @@ struct DevBuf {
   }
   int ensure(size_t n);                     // grow-only, cudaMalloc
   int ensure_on(size_t n, cudaStream_t s);  // grow-only, cudaMallocAsync on s (pool)
+  // grow-only pool allocation for scratch used on arbitrary streams: a grow
+  // synchronizes the device first, teardown frees synchronously — so a
+  // rebuilt graph reuses pool memory instead of paying cudaMalloc again
+  int ensure_pooled(size_t n, cudaStream_t s);
   template <class T> T *as() const { return static_cast<T *>(p); }
 };
 
@@ -203,7 +207,7 @@ struct tm_graph {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   // host-output pieces: D2H of piece i overlaps mining of piece i+1
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t piece_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t piece_ev[8] = {};
   tmb::DevBuf split_counts;
 
   tmb::DevGraph dev() const;
