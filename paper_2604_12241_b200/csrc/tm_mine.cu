@@ -646,7 +646,17 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
   const int64_t left = n_rows - wrow0;
   const int nrow = left < 32 ? (int)(left > 0 ? left : 0) : 32;
   long long *dst = out + wrow0 * C;
-  for (int i = lane; i < nrow * S; i += 32) dst[(i / S) * C + P.slot_col[i % S]] = stage[i];
+  if (S == 0) return;
+  // staged cells i = r * S + k, dealt 32 at a time; (r, k) advanced
+  // incrementally instead of dividing by the runtime S
+  const int dq = 32 / S, dr = 32 % S;
+  int r0 = lane / S, k0 = lane % S;
+  for (int i = lane; i < nrow * S; i += 32) {
+    dst[r0 * C + P.slot_col[k0]] = stage[i];
+    r0 += dq;
+    k0 += dr;
+    if (k0 >= S) k0 -= S, ++r0;
+  }
 }
 
 // ------------------------------------------------------------ tasks
