@@ -75,11 +75,35 @@ struct Task {
   int32_t path[kMaxChain];  // chain a1..a_level; domain tasks: path[0] = scratch slot
 };
 
+// Backward-layer filters of the trigger a task works for (task kernel; see
+// TaskBloom): the chain walk skips nodes that cannot reach u in time
+struct TaskBloom;
+
 struct Queue {
   Task *q;
   int32_t *count;
   int32_t cap;
+  const TaskBloom *bloom;  // null: no filtering (warp kernel, small windows)
 };
+
+// Bloom filters of the backward layers B_2 and B_3 (B_1 = N-(u) \ {u, v},
+// B_{k+1} = N-(B_k) \ {u, v}, windowed): a node at depth j that closes at
+// depth d lies in B_{2+d-j}, so a chain task over a hub window (long delta:
+// millions of chain nodes) tests each candidate against the layers its
+// depth needs before reading its window.  No false negatives, so the walk
+// stays exact; a layer that could not be built completely is "all".
+constexpr int kBloomWords = 64;  // 2048 bits per layer
+constexpr int kB2Cap = 512;      // B_2 members kept to build B_3
+struct TaskBloom {
+  uint32_t w[2][kBloomWords];
+  int32_t n2, valid3;
+  int32_t list[kB2Cap];
+};
+__device__ __forceinline__ uint32_t bloom_bit(int x) { return ((uint32_t)x * 0x9E3779B1u) >> 21; }
+__device__ __forceinline__ bool bloom_has(const uint32_t *w, int x) {
+  const uint32_t b = bloom_bit(x);
+  return (w[b >> 5] >> (b & 31)) & 1u;
+}
 
 // cut [a, b) into kTaskSpan pieces; false (caller walks it itself) when the
 // queue is full — the walk is slower but exact and still on the GPU
@@ -326,9 +350,29 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
     os = __ldg(c.g.ptr[1] + owner);
     oe = __ldg(c.g.ptr[1] + owner + 1);
   }
+  // layers a depth-(L+1) node must meet: B_{1+d-L} for closing depths d
+  int need = 0;
+  bool filter = false;
+  if constexpr (PI) {
+    if (qu.bloom) {
+      filter = true;
+      for (int d = L + 1; d <= MAXD; ++d) {
+        if (!(cg.mask & (1 << d))) continue;
+        const int k = 1 + d - L;
+        if (k == 2) need |= 1;
+        else if (k == 3) need |= qu.bloom->valid3 ? 2 : 4;
+        else need |= 4;  // deeper layers are not filtered
+      }
+    }
+  }
   for (int j = ja; j < jb; ++j) {
     const int a = cand ? cand[j] : __ldg(c.g.nbr[1] + j);
     if (a == owner || a == c.u || a == c.v) continue;
+    if constexpr (PI) {
+      if (filter && !(need & 4) &&
+          !(((need & 1) && bloom_has(qu.bloom->w[0], a)) || ((need & 2) && bloom_has(qu.bloom->w[1], a))))
+        continue;
+    }
     bool dup = false;
 #pragma unroll
     for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
@@ -720,6 +764,44 @@ __device__ __forceinline__ bool pull_gs(const Ctx &c, const DevPlans &P, const D
   return __shfl_sync(0xffffffffu, ok, 0);
 }
 
+// the task's backward-layer filters, built by the warp: lanes split B_1's
+// in-windows (B_2 bits + list), then B_2's (B_3 bits)
+__device__ void build_bloom(const Ctx &c, TaskBloom &B, int lane) {
+  __syncwarp();  // lanes may still be reading the previous task's filters
+  for (int i = lane; i < 2 * kBloomWords; i += 32) (&B.w[0][0])[i] = 0u;
+  if (lane == 0) {
+    B.n2 = 0;
+    B.valid3 = 1;
+  }
+  __syncwarp();
+  for (int j = c.wui.a + lane; j < c.wui.b; j += 32) {
+    const int m1 = __ldg(c.g.nbr[0] + j);
+    if (m1 == c.u || m1 == c.v || !first_in_window(c, 0, j)) continue;
+    const Win w = window(c, 0, m1);
+    for (int k = w.a; k < w.b; ++k) {
+      const int m2 = __ldg(c.g.nbr[0] + k);
+      if (m2 == c.u || m2 == c.v || !first_in_window(c, 0, k)) continue;
+      const uint32_t b = bloom_bit(m2);
+      atomicOr(&B.w[0][b >> 5], 1u << (b & 31));
+      const int idx = atomicAdd(&B.n2, 1);
+      if (idx < kB2Cap) B.list[idx] = m2;
+      else B.valid3 = 0;
+    }
+  }
+  __syncwarp();
+  const int n2 = min(B.n2, kB2Cap);
+  for (int i = lane; i < n2; i += 32) {
+    const Win w = window(c, 0, B.list[i]);
+    for (int k = w.a; k < w.b; ++k) {
+      const int m3 = __ldg(c.g.nbr[0] + k);
+      if (m3 == c.u || m3 == c.v || !first_in_window(c, 0, k)) continue;
+      const uint32_t b = bloom_bit(m3);
+      atomicOr(&B.w[1][b >> 5], 1u << (b & 31));
+    }
+  }
+  __syncwarp();
+}
+
 // Task kinds (one warp per task):
 //   kLvlDomU / kLvlDomV   a piece of a trigger's U / V slice, lane per entry
 //   kLvlPullV             a hub v's whole N+(v): gs from u's side (pull_gs),
@@ -732,10 +814,12 @@ __device__ __forceinline__ bool pull_gs(const Ctx &c, const DevPlans &P, const D
 // Each kind feeds ONE call site of the item / chain code below.
 __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
-    long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next) {
+    long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q) {
   const int n = min(*in.count, in.cap);
   const int warps = gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
+  __shared__ TaskBloom blooms[kTaskThreads / 32];
+  TaskBloom &bloom = blooms[threadIdx.x >> 5];
   for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
     const Task t = in.q[i];
     if (t.row < 0) continue;
@@ -744,6 +828,13 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     const uint32_t r = __ldg(g.e_rank + e);
     Ctx c{g, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {}};
     trigger_windows(c, gr, t.row);
+    // chain walks of this task get the trigger's backward-layer filters
+    Queue next = next_q;
+    const bool chains = t.level != kLvlDomU && !(t.level == kLvlDomV && !(t.pad0 & kVCyc));
+    if (chains && gr.cyc.maxd >= 2 && c.u != c.v && c.wui.len() > 0) {
+      build_bloom(c, bloom, lane);
+      next.bloom = &bloom;
+    }
     long long *orow = out + (int64_t)t.row * P.n;
     int use[kBCap];
     if (t.level == kLvlDomU) {
@@ -1032,8 +1123,8 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     return rc;
   int32_t *cnt = g->heavy_n.as<int32_t>();  // [0] split rows, [1] [2] task queues A / B
   TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
-  Queue qa{g->tasks.as<Task>(), cnt + 1, (int32_t)task_cap};
-  Queue qb{g->tasks.as<Task>() + task_cap, cnt + 2, (int32_t)task_cap};
+  Queue qa{g->tasks.as<Task>(), cnt + 1, (int32_t)task_cap, nullptr};
+  Queue qb{g->tasks.as<Task>() + task_cap, cnt + 2, (int32_t)task_cap, nullptr};
 
   for (int i = 0; i < n_plans; ++i) {
     const int f = plans[i].family;
