@@ -150,6 +150,14 @@ __device__ __forceinline__ bool first_in_window(const Ctx &c, int dir, int j) {
   return __ldg(c.g.prev[dir] + j) <= c.lo;
 }
 
+// (neighbour, prev) of CSR slot j in one 8-byte load: the walkers read both
+// for every entry (membership test + np.unique dedup)
+__device__ __forceinline__ int2 slot_np(const Ctx &c, int dir, int j) {
+  TM_CNT(kCtrFirst, 1);
+  return __ldg(c.g.np[dir] + j);
+}
+__device__ __forceinline__ bool first_of(const Ctx &c, int2 sl) { return (uint32_t)sl.y <= c.lo; }
+
 // does x's dir-window w contain neighbour n?  Windows are time-local and
 // short: scan them.  A wide w (a hub) is answered by one bisection of the
 // SHORTER pair run: x's dir run keyed by n, or n's opposite run keyed by x

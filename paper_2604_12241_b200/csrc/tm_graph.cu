@@ -135,6 +135,12 @@ __global__ void k_pair_fill(const uint64_t *__restrict__ pair_sorted, const uint
   prev[p] = (q > 0 && pair_sorted[q - 1] == pair_sorted[q]) ? rnk[pids[q - 1]] + 1u : 0u;
 }
 
+__global__ void k_np_fill(const int32_t *__restrict__ nbr, const uint32_t *__restrict__ prev, int64_t n,
+                          int2 *__restrict__ np) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) np[p] = make_int2(nbr[p], (int)prev[p]);
+}
+
 __global__ void k_max_degree(const int32_t *__restrict__ ptr, int64_t n_nodes,
                              unsigned long long *out) {
   unsigned long long m = 0;
@@ -223,6 +229,7 @@ tmb::DevGraph tm_graph::dev() const {
     g.prev[d] = prev[d].as<uint32_t>();
     g.eid[d] = eid[d].as<int32_t>();
     g.peid[d] = peid[d].as<int32_t>();
+    g.np[d] = npk[d].as<int2>();
   }
   g.loop = loop.as<uint8_t>();
   return g;
@@ -260,7 +267,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
     if ((rc = g->ptr[d].ensure_on(4 * (N + 1), s)) || (rc = g->nbr[d].ensure_on(4 * Ea, s)) ||
         (rc = g->rnk[d].ensure_on(4 * Ea, s)) || (rc = g->eid[d].ensure_on(4 * Ea, s)) ||
         (rc = g->pkey[d].ensure_on(8 * Ea, s)) || (rc = g->prev[d].ensure_on(4 * Ea, s)) ||
-        (rc = g->peid[d].ensure_on(4 * Ea, s)))
+        (rc = g->peid[d].ensure_on(4 * Ea, s)) || (rc = g->npk[d].ensure_on(8 * Ea, s)))
       return rc;
   }
   if (E == 0) {
@@ -358,6 +365,9 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
                                                g->rank_bits, g->pkey[d].as<uint64_t>(),
                                                g->prev[d].as<uint32_t>(), g->peid[d].as<int32_t>());
     TM_LAUNCHED("k_pair_fill");
+    k_np_fill<<<grid_for(E, kB), kB, 0, s>>>(g->nbr[d].as<int32_t>(), g->prev[d].as<uint32_t>(), E,
+                                             g->npk[d].as<int2>());
+    TM_LAUNCHED("k_np_fill");
     unsigned long long *md = g->maxdeg.as<unsigned long long>() + d;  // read lazily by info
     TM_CUDA(cudaMemsetAsync(md, 0, 8, s));
     k_max_degree<<<592, kB, 0, s>>>(g->ptr[d].as<int32_t>(), N, md);
@@ -411,7 +421,8 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
   for (const DevBuf *b : {&g->e_src, &g->e_dst, &g->e_rank, &g->uniq_time, &g->loop})
     bytes += (int64_t)b->bytes;
   for (int d = 0; d < 2; ++d)
-    for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d], &g->peid[d]})
+    for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d], &g->peid[d],
+                            &g->npk[d]})
       bytes += (int64_t)b->bytes;
   g->device_bytes = bytes;
   *out = g;

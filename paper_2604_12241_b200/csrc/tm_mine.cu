@@ -174,8 +174,9 @@ __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, in
   if (xe - xs > kLazyRun && wy.len() <= kLazyRun) {
     for (int j = wy.a; j < wy.b && hits < K; ++j) {
       TM_CNT(kCtrInnerWalk, 1);
-      const int m = __ldg(c.g.nbr[dy] + j);
-      if (m == x || m == y || m == f || !first_in_window(c, dy, j)) continue;
+      const int2 sl = slot_np(c, dy, j);
+      const int m = sl.x;
+      if (m == x || m == y || m == f || !first_of(c, sl)) continue;
       hits += exists_pair(c, dx, x, xs, xe, m);
     }
     return hits;
@@ -190,8 +191,9 @@ __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, in
   const Win ow = walk_x ? wy : wx;
   for (int j = w.a; j < w.b && hits < K; ++j) {
     TM_CNT(kCtrInnerWalk, 1);
-    const int m = __ldg(c.g.nbr[d] + j);
-    if (m == x || m == y || m == f || !first_in_window(c, d, j)) continue;
+    const int2 sl = slot_np(c, d, j);
+    const int m = sl.x;
+    if (m == x || m == y || m == f || !first_of(c, sl)) continue;
     hits += exists_in(c, od, other, ow, m);
   }
   return hits;
@@ -210,12 +212,13 @@ __device__ __forceinline__ int close_count(const Ctx &c, int a, const Win &wa,
   TM_CNT(kCtrCloseCall, 1);
   for (int j = w.a; j < w.b; ++j) {
     TM_CNT(kCtrCloseWalk, 1);
-    const int m = __ldg(c.g.nbr[d] + j);
+    const int2 sl = slot_np(c, d, j);
+    const int m = sl.x;
     if (m == a || m == c.u || m == c.v) continue;
     bool dup = false;
 #pragma unroll
     for (int i = 0; i < NP; ++i) dup |= (path[i] == m);
-    if (dup || !first_in_window(c, d, j)) continue;
+    if (dup || !first_of(c, sl)) continue;
     cnt += walk_a ? exists_in(c, 0, c.u, c.wui, m) : exists_in(c, 1, a, wa, m);
   }
   return cnt;
@@ -366,7 +369,8 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
     }
   }
   for (int j = ja; j < jb; ++j) {
-    const int a = cand ? cand[j] : __ldg(c.g.nbr[1] + j);
+    const int2 sl = cand ? make_int2(cand[j], 0) : slot_np(c, 1, j);
+    const int a = sl.x;
     if (a == owner || a == c.u || a == c.v) continue;
     if constexpr (PI) {
       if (filter && !(need & 4) &&
@@ -376,7 +380,7 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
     bool dup = false;
 #pragma unroll
     for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
-    if (dup || !(cand ? exists_pair(c, 1, owner, os, oe, a) : first_in_window(c, 1, j))) continue;
+    if (dup || !(cand ? exists_pair(c, 1, owner, os, oe, a) : first_of(c, sl))) continue;
     chain_pick<MAXD, L, PI>(c, cg, row, grp, path, a, acc, qu);
   }
 }
@@ -441,9 +445,10 @@ __device__ __forceinline__ void cycles_resume(const Ctx &c, const CycGroup &cg, 
 template <class Sink>
 __device__ __forceinline__ void u_item(const Ctx &c, const DevPlans &P, const DevGroup &gr, int j,
                                        Sink &sk) {
-  const int m = __ldg(c.g.nbr[0] + j);
+  const int2 sl = slot_np(c, 0, j);
+  const int m = sl.x;
   TM_CNT(kCtrUWalk, 1);
-  if (m == c.u || m == c.v || !first_in_window(c, 0, j)) return;
+  if (m == c.u || m == c.v || !first_of(c, sl)) return;
   TM_CNT(kCtrUItem, 1);
   if (gr.has_stack) sk.sa();
   if ((gr.cyc.mask & 1) && c.u != c.v && exists_in(c, 1, c.v, c.wvo, m)) sk.c3();
@@ -657,9 +662,10 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
       const Ctx co = ctx_of(g, ws, o);
       SmemSink sk{ws, stage, P.slot, o, S};
       const int j = co.wvo.a + k;
-      const int m = __ldg(g.nbr[1] + j);
+      const int2 sl = slot_np(co, 1, j);
+      const int m = sl.x;
       TM_CNT(kCtrVWalk, 1);
-      if (m == co.u || m == co.v || !first_in_window(co, 1, j)) return;
+      if (m == co.u || m == co.v || !first_of(co, sl)) return;
       v_node<false>(co, P, gr, gi, ws.rowid[o], m, sk, qu, ws.c3[o] >> kPartsShift);
     });
     // whole-count columns: stack a * c (kernels.py:379-402), cycle_3 threshold
@@ -884,8 +890,9 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
           m = cand[k];
           if (m == c.u || m == c.v || !exists_pair(c, 1, c.v, vs, ve, m)) continue;
         } else {
-          m = __ldg(g.nbr[1] + k);
-          if (m == c.u || m == c.v || !first_in_window(c, 1, k)) continue;
+          const int2 sl = slot_np(c, 1, k);
+          m = sl.x;
+          if (m == c.u || m == c.v || !first_of(c, sl)) continue;
         }
         v_node<true>(c, P, gr, t.grp, t.row, m, sk, next, parts);
       }
