@@ -154,9 +154,11 @@ __device__ __forceinline__ void fill_windows(Ctx &c, int need) {
 #endif
 }
 
-// self-loops of x inside the window (kernels.py:279-287): pair run (x, x)
-__device__ __forceinline__ int loops_in_window(const Ctx &c, int x) {
-  if (!__ldg(c.g.loop + x)) return 0;
+// self-loops of x inside the window (kernels.py:279-287): pair run (x, x);
+// has_loop = loop[x] when the caller already holds it
+__device__ __forceinline__ int loops_in_window(const Ctx &c, int x, int has_loop = -1) {
+  if (has_loop < 0) has_loop = __ldg(c.g.loop + x);
+  if (!has_loop) return 0;
   const int a = __ldg(c.g.ptr[1] + x), b = __ldg(c.g.ptr[1] + x + 1);
   const uint64_t base = (uint64_t)(uint32_t)x << c.g.rank_bits;
   return lb_u64(c.g.pkey[1], a, b, base + c.hi + 1) - lb_u64(c.g.pkey[1], a, b, base + c.lo);

@@ -597,13 +597,14 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     if (valid) trigger_windows(c, gr, (int)row);
     // per-lane columns: fan / degree (kernels.py:290-303), cycle_2 (:320-322)
     if (valid) {
+      const int loop_u = __ldg(g.loop + u), loop_v = __ldg(g.loop + v);  // once, not per column
       for (int i = 0; i < gr.ncols; ++i) {
         const int ci = gr.cols[i];
         const DevPlan &p = P.p[ci];
         if (p.family == TM_FAN || p.family == TM_DEGREE) {
           const int x = p.endpoint ? v : u;
           const Win w = p.endpoint ? (p.direction ? c.wvo : c.wvi) : (p.direction ? c.wuo : c.wui);
-          long long n = w.len() - loops_in_window(c, x);
+          long long n = w.len() - loops_in_window(c, x, p.endpoint ? loop_v : loop_u);
           if (p.exclude_trigger && u != v) n -= 1;
           if (p.min_size > 1 && n < p.min_size) n = 0;
           orow[ci] = n;
