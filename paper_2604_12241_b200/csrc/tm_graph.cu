@@ -95,7 +95,7 @@ __global__ void k_csr_fill(const uint64_t *__restrict__ keys, const uint32_t *__
                            const int32_t *__restrict__ other, int64_t n, int rbits,
                            int32_t *__restrict__ nbr, uint32_t *__restrict__ rnk,
                            int32_t *__restrict__ eid, uint64_t *__restrict__ pair_keys,
-                           uint32_t *__restrict__ pair_ids, int nbits) {
+                           uint32_t *__restrict__ pair_ids, int nbits, int32_t *__restrict__ own) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint64_t key = keys[p];
@@ -103,6 +103,7 @@ __global__ void k_csr_fill(const uint64_t *__restrict__ keys, const uint32_t *__
   const int32_t o = other[e];
   const uint64_t owner = key >> rbits;
   nbr[p] = o;
+  own[p] = (int32_t)owner;
   rnk[p] = (uint32_t)(key & ((1ull << rbits) - 1));
   eid[p] = (int32_t)e;
   pair_keys[p] = (owner << nbits) | (uint32_t)o;
@@ -230,6 +231,7 @@ tmb::DevGraph tm_graph::dev() const {
     g.eid[d] = eid[d].as<int32_t>();
     g.peid[d] = peid[d].as<int32_t>();
     g.np[d] = npk[d].as<int2>();
+    g.owner[d] = owner[d].as<int32_t>();
   }
   g.loop = loop.as<uint8_t>();
   return g;
@@ -267,7 +269,8 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
     if ((rc = g->ptr[d].ensure_on(4 * (N + 1), s)) || (rc = g->nbr[d].ensure_on(4 * Ea, s)) ||
         (rc = g->rnk[d].ensure_on(4 * Ea, s)) || (rc = g->eid[d].ensure_on(4 * Ea, s)) ||
         (rc = g->pkey[d].ensure_on(8 * Ea, s)) || (rc = g->prev[d].ensure_on(4 * Ea, s)) ||
-        (rc = g->peid[d].ensure_on(4 * Ea, s)) || (rc = g->npk[d].ensure_on(8 * Ea, s)))
+        (rc = g->peid[d].ensure_on(4 * Ea, s)) || (rc = g->npk[d].ensure_on(8 * Ea, s)) ||
+        (rc = g->owner[d].ensure_on(4 * Ea, s)))
       return rc;
   }
   if (E == 0) {
@@ -353,7 +356,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
     uint32_t *pv = (vs == va.as<uint32_t>()) ? vb.as<uint32_t>() : va.as<uint32_t>();
     k_csr_fill<<<grid_for(E, kB), kB, 0, s>>>(ks, vs, other, E, g->rank_bits, g->nbr[d].as<int32_t>(),
                                               g->rnk[d].as<uint32_t>(), g->eid[d].as<int32_t>(), pk,
-                                              pv, g->node_bits);
+                                              pv, g->node_bits, g->owner[d].as<int32_t>());
     TM_LAUNCHED("k_csr_fill");
     uint64_t *ps;
     uint32_t *pvs;
@@ -422,7 +425,7 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
     bytes += (int64_t)b->bytes;
   for (int d = 0; d < 2; ++d)
     for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d], &g->peid[d],
-                            &g->npk[d]})
+                            &g->npk[d], &g->owner[d]})
       bytes += (int64_t)b->bytes;
   g->device_bytes = bytes;
   *out = g;

@@ -52,6 +52,7 @@ struct DevGraph {
   const int32_t *eid[2];   // edge id per CSR slot (members attribution)
   const int32_t *peid[2];  // edge id per pair slot (members attribution)
   const int2 *np[2];       // (nbr, prev) per CSR slot, interleaved for the walkers
+  const int32_t *owner[2]; // owner node of each CSR slot (slot-parallel window sweeps)
   const uint8_t *loop;
 };
 
@@ -190,7 +191,7 @@ struct tm_graph {
   int64_t device_bytes = 0;
 
   tmb::DevBuf e_src, e_dst, e_rank, uniq_time, loop, maxdeg;
-  tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2], peid[2], npk[2];
+  tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2], peid[2], npk[2], owner[2];
 
   // mining scratch (grow-only)
   tmb::DevBuf lo_tabs, own_tabs, heavy_q, heavy_n, out_scratch, tasks, split_scratch;

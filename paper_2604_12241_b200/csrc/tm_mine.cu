@@ -979,7 +979,7 @@ __global__ void k_own_windows(const __grid_constant__ DevGraph g, const uint32_t
   if (p >= g.n_edges) return;
   const int e = __ldg(g.eid[dir] + p);
   if (e < lo || e >= hi) return;
-  const int x = dir ? __ldg(g.e_src + e) : __ldg(g.e_dst + e);
+  const int x = __ldg(g.owner[dir] + p);  // coalesced (was a gather through the edge table)
   const int a = __ldg(g.ptr[dir] + x), b = __ldg(g.ptr[dir] + x + 1);
   const uint32_t *rk = g.rnk[dir];
   const uint32_t r = __ldg(rk + p);
