@@ -177,7 +177,7 @@ int DevBuf::ensure_on(size_t n, cudaStream_t s) {
   return TM_OK;
 }
 
-int DevBuf::ensure_pooled(size_t n, cudaStream_t s) {
+int DevBuf::ensure_pooled(size_t n, cudaStream_t s, cudaStream_t free_stream) {
   if (n <= bytes && p) return TM_OK;
   if (p) {
     cudaDeviceSynchronize();  // earlier calls on other streams may still use the old block
@@ -193,7 +193,7 @@ int DevBuf::ensure_pooled(size_t n, cudaStream_t s) {
   }
   bytes = n ? n : 16;
   pooled = true;
-  pool_stream = nullptr;
+  pool_stream = free_stream;  // the graph's own stream: teardown frees back into the pool
   return TM_OK;
 }
 

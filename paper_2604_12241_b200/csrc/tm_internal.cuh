@@ -149,9 +149,10 @@ struct DevBuf {
   int ensure(size_t n);                     // grow-only, cudaMalloc
   int ensure_on(size_t n, cudaStream_t s);  // grow-only, cudaMallocAsync on s (pool)
   // grow-only pool allocation for scratch used on arbitrary streams: a grow
-  // synchronizes the device first, teardown frees synchronously — so a
+  // synchronizes the device first; frees are stream-ordered on free_stream
+  // (the graph's stream; teardown synchronizes the device before) — so a
   // rebuilt graph reuses pool memory instead of paying cudaMalloc again
-  int ensure_pooled(size_t n, cudaStream_t s);
+  int ensure_pooled(size_t n, cudaStream_t s, cudaStream_t free_stream);
   template <class T> T *as() const { return static_cast<T *>(p); }
 };
 

@@ -1087,14 +1087,14 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   }
   const int64_t R = g->n_ranks;
   int rc;
-  if ((rc = g->lo_tabs.ensure_pooled(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups, s))) return rc;
+  if ((rc = g->lo_tabs.ensure_pooled(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups, s, g->stream))) return rc;
   // own-window tables pay off when a group needs them for many triggers
   const int64_t E = g->n_edges;
   const bool own_on = own_windows_enabled() && rows * 64 >= E;
   int n_own = 0;
   if (own_on)
     for (int k = 0; k < dp.ngroups; ++k) n_own += ((dp.gr[k].need >> 1) & 1) + ((dp.gr[k].need >> 2) & 1);
-  if (n_own && (rc = g->own_tabs.ensure_pooled(sizeof(int2) * (size_t)rows * n_own, s))) return rc;
+  if (n_own && (rc = g->own_tabs.ensure_pooled(sizeof(int2) * (size_t)rows * n_own, s, g->stream))) return rc;
   const DevGraph dg = g->dev();
   int rounds = 0;
   int own_i = 0;
@@ -1119,15 +1119,15 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   if (out_on_device) {
     d_out = reinterpret_cast<long long *>(out);
   } else {
-    if ((rc = g->out_scratch.ensure_pooled(sizeof(long long) * (size_t)rows * n_plans, s))) return rc;
+    if ((rc = g->out_scratch.ensure_pooled(sizeof(long long) * (size_t)rows * n_plans, s, g->stream))) return rc;
     d_out = g->out_scratch.as<long long>();
   }
   const int64_t task_cap = std::min<int64_t>(std::max<int64_t>(1 << 18, rows / 8), 1 << 24);
   const int64_t split_cap = std::min<int64_t>(std::max<int64_t>(1 << 16, rows / 16), 1 << 22);
-  if ((rc = g->heavy_n.ensure_pooled(sizeof(int32_t) * 4, s)) ||
-      (rc = g->heavy_q.ensure_pooled(sizeof(int32_t) * 2 * (size_t)split_cap, s)) ||
-      (rc = g->split_scratch.ensure_pooled(sizeof(int32_t) * 3 * (size_t)split_cap, s)) ||
-      (rc = g->tasks.ensure_pooled(sizeof(Task) * (size_t)task_cap * 2, s)))
+  if ((rc = g->heavy_n.ensure_pooled(sizeof(int32_t) * 4, s, g->stream)) ||
+      (rc = g->heavy_q.ensure_pooled(sizeof(int32_t) * 2 * (size_t)split_cap, s, g->stream)) ||
+      (rc = g->split_scratch.ensure_pooled(sizeof(int32_t) * 3 * (size_t)split_cap, s, g->stream)) ||
+      (rc = g->tasks.ensure_pooled(sizeof(Task) * (size_t)task_cap * 2, s, g->stream)))
     return rc;
   int32_t *cnt = g->heavy_n.as<int32_t>();  // [0] split rows, [1] [2] task queues A / B
   TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
@@ -1160,7 +1160,7 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     for (int i = 0; i < kHostPieces; ++i)
       TM_CUDA(cudaEventCreateWithFlags(&g->piece_ev[i], cudaEventDisableTiming));
   }
-  if ((rc = g->split_counts.ensure_pooled(sizeof(int32_t) * kHostPieces, s))) return rc;
+  if ((rc = g->split_counts.ensure_pooled(sizeof(int32_t) * kHostPieces, s, g->stream))) return rc;
   int32_t *piece_split = g->split_counts.as<int32_t>();
   g->prof_pending = g->prof;
   if (g->prof) TM_CUDA(cudaEventRecord(g->ev[0], s));

@@ -141,6 +141,22 @@ def test_powerlaw_hubs_vs_oracle(tmb):
         assert st.heavy_triggers > 0  # the warp path was exercised
 
 
+def test_long_windows_pull_and_filters_vs_oracle(tmb):
+    """Long windows over power-law hubs: the backward sets overflow their
+    exact lists, so chain tasks run with the B2/B3 Bloom filters; hub v
+    triggers take the pull-V path (gs from u's side, cycles via useful a1);
+    sg/gs thresholds 2 and 3 exercise the probe-free hits."""
+    from paper_2604_12241_b200 import synth
+    cfg = synth.SynthConfig(2500, 50000, 8 * 86400, seed=23, powerlaw_exponent=1.0,
+                            plants=(synth.PlantSpec("cycle_4", 20), synth.PlantSpec("sg_count", 20)))
+    g0 = synth.generate(cfg)
+    names = ["cycle_3", "cycle_4", "cycle_5", "cycle_6", "sg_count", "gs_count", "stack_count",
+             "gs_count", "sg_count"]
+    ks = [None, None, None, None, None, None, None, 3, 3]
+    st = _oracle_vs_gpu(tmb, g0.src, g0.dst, g0.time, 3 * 86400, names=names, ks=ks)
+    assert st.heavy_triggers > 0
+
+
 def test_dense_small_graph_vs_oracle(tmb):
     """Dense windows: long cycle chains, large intersections, self-loops."""
     rng = np.random.default_rng(21)

@@ -8,6 +8,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import os
+if len(sys.argv) > 3:
+    os.environ["TM_LIB"] = os.path.abspath(sys.argv[3])
 import paper_2604_12241_b200 as tmb  # noqa: E402
 from paper_2604_12241_b200 import synth  # noqa: E402
 
@@ -17,7 +20,7 @@ pin = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).pin_me
 hs, hd, ht = pin(g0.src), pin(g0.dst), pin(g0.time)
 descs = [tmb.lower_plan(p) for p in tmb.full_pattern_set(86400)]
 hout = torch.empty((g0.edge_count, len(descs)), dtype=torch.int64).pin_memory().numpy()
-for rep in range(4):
+for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 4):
     t0 = time.perf_counter()
     g = tmb.DeviceGraph(hs, hd, ht, node_count=g0.node_count)
     t1 = time.perf_counter()
