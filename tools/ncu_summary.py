@@ -32,7 +32,8 @@ METRICS = {
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-              "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+              "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+              "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
 def raw(rep: str):
