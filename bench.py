@@ -336,6 +336,7 @@ def main():
             em = float(t.item())
         e2e = {"value": E / (em / 1e3), "unit": UNIT, "h2d_bytes_per_step": 24 * E * world,
                "d2h_bytes_per_step": 8 * E * C, "ms_per_step": em,
+               "step_ms": [round(x, 3) for x in e2e_ms], "median_ms": float(np.median(e2e_ms)),
                "includes": "H2D of src/dst/time (pinned), GPU CSR build, mining, D2H of the int64 "
                            "feature block (pinned)"}
     cpu = None

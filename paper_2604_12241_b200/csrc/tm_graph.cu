@@ -7,6 +7,7 @@
 // of packed (owner << rank_bits | rank) keys over an eid-ordered input, and
 // indptr from run boundaries of the sorted keys (no atomics on hub nodes).
 #include <algorithm>
+#include <mutex>
 #include <cstring>
 #include <vector>
 
@@ -408,12 +409,26 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
   if (stream) {
     g->stream = static_cast<cudaStream_t>(stream);
   } else {
-    cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
+    // one persistent library stream per device: graphs rebuilt in a loop
+    // allocate and free on the same stream, so the memory pool hands the
+    // previous graph's blocks straight back (no new physical mappings)
+    static std::mutex mu;
+    static cudaStream_t lib_stream[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (device >= 64) {
       delete g;
-      return cuda_fail(e, "cudaStreamCreate");
+      return fail(TM_E_BAD_ARG, "device ordinal >= 64");
     }
-    g->owns_stream = true;
+    if (!lib_stream[device]) {
+      cudaError_t e = cudaStreamCreateWithFlags(&lib_stream[device], cudaStreamNonBlocking);
+      if (e != cudaSuccess) {
+        lib_stream[device] = nullptr;
+        delete g;
+        return cuda_fail(e, "cudaStreamCreate");
+      }
+    }
+    g->stream = lib_stream[device];
+    g->owns_stream = false;
   }
   int rc = build_impl(g, src, dst, time, inputs_on_device);
   if (rc) {
