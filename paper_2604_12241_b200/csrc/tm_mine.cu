@@ -86,20 +86,22 @@ struct Queue {
   const TaskBloom *bloom;  // null: no filtering (warp kernel, small windows)
 };
 
-// Bloom filters of the backward layers B_2 and B_3 (B_1 = N-(u) \ {u, v},
+// Bloom filters of the backward layers B_2..B_5 (B_1 = N-(u) \ {u, v},
 // B_{k+1} = N-(B_k) \ {u, v}, windowed): a node at depth j that closes at
-// depth d lies in B_{2+d-j}, so a chain task over a hub window (long delta:
+// depth d lies in B_{2+d-j}, so a chain walk over a hub window (long delta:
 // millions of chain nodes) tests each candidate against the layers its
 // depth needs before reading its window.  No false negatives, so the walk
 // stays exact; a layer that could not be built completely is "all".
-constexpr int kBloomWords = 64;  // 2048 bits per layer
-constexpr int kB2Cap = 512;      // B_2 members kept to build B_3
+constexpr int kBloomLayers = 4;    // B_2 .. B_5
+constexpr int kBloomWords = 256;   // 8192 bits per layer
+constexpr int kBloomList = 4096;   // members of one layer kept to build the next (global scratch)
+constexpr int kInPlace = 4096;     // a filtered pull task walks windows up to this long itself
 struct TaskBloom {
-  uint32_t w[2][kBloomWords];
-  int32_t n2, valid3;
-  int32_t list[kB2Cap];
+  uint32_t w[kBloomLayers][kBloomWords];
+  int32_t valid;  // bit k-2: layer B_k complete
+  int32_t n[2];   // list fill counters (ping-pong)
 };
-__device__ __forceinline__ uint32_t bloom_bit(int x) { return ((uint32_t)x * 0x9E3779B1u) >> 21; }
+__device__ __forceinline__ uint32_t bloom_bit(int x) { return ((uint32_t)x * 0x9E3779B1u) >> 19; }
 __device__ __forceinline__ bool bloom_has(const uint32_t *w, int x) {
   const uint32_t b = bloom_bit(x);
   return (w[b >> 5] >> (b & 31)) & 1u;
@@ -358,14 +360,13 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
   bool filter = false;
   if constexpr (PI) {
     if (qu.bloom) {
-      filter = true;
       for (int d = L + 1; d <= MAXD; ++d) {
         if (!(cg.mask & (1 << d))) continue;
         const int k = 1 + d - L;
-        if (k == 2) need |= 1;
-        else if (k == 3) need |= qu.bloom->valid3 ? 2 : 4;
-        else need |= 4;  // deeper layers are not filtered
+        if (k - 2 < kBloomLayers && ((qu.bloom->valid >> (k - 2)) & 1)) need |= 1 << (k - 2);
+        else need |= 1 << kBloomLayers;  // not filtered
       }
+      filter = !(need >> kBloomLayers);
     }
   }
   for (int j = ja; j < jb; ++j) {
@@ -373,9 +374,13 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
     const int a = sl.x;
     if (a == owner || a == c.u || a == c.v) continue;
     if constexpr (PI) {
-      if (filter && !(need & 4) &&
-          !(((need & 1) && bloom_has(qu.bloom->w[0], a)) || ((need & 2) && bloom_has(qu.bloom->w[1], a))))
-        continue;
+      if (filter) {
+        bool hit = false;
+#pragma unroll
+        for (int k = 0; k < kBloomLayers; ++k)
+          if ((need >> k) & 1) hit |= bloom_has(qu.bloom->w[k], a);
+        if (!hit) continue;
+      }
     }
     bool dup = false;
 #pragma unroll
@@ -771,42 +776,53 @@ __device__ __forceinline__ bool pull_gs(const Ctx &c, const DevPlans &P, const D
   return __shfl_sync(0xffffffffu, ok, 0);
 }
 
-// the task's backward-layer filters, built by the warp: lanes split B_1's
-// in-windows (B_2 bits + list), then B_2's (B_3 bits)
-__device__ void build_bloom(const Ctx &c, TaskBloom &B, int lane) {
+// the task's backward-layer filters B_2..B_top, built by the warp: lanes
+// split the previous layer's members (B_1 = u's in-window), expand their
+// in-windows, set bits and list the members for the next layer (global
+// ping-pong lists); a layer whose list overflows ends the build
+__device__ void build_bloom(const Ctx &c, TaskBloom &B, int lane, int top, int *list0, int *list1) {
   __syncwarp();  // lanes may still be reading the previous task's filters
-  for (int i = lane; i < 2 * kBloomWords; i += 32) (&B.w[0][0])[i] = 0u;
+  for (int i = lane; i < kBloomLayers * kBloomWords; i += 32) (&B.w[0][0])[i] = 0u;
   if (lane == 0) {
-    B.n2 = 0;
-    B.valid3 = 1;
+    B.valid = 0;
+    B.n[0] = B.n[1] = 0;
   }
   __syncwarp();
-  for (int j = c.wui.a + lane; j < c.wui.b; j += 32) {
-    const int m1 = __ldg(c.g.nbr[0] + j);
-    if (m1 == c.u || m1 == c.v || !first_in_window(c, 0, j)) continue;
-    const Win w = window(c, 0, m1);
-    for (int k = w.a; k < w.b; ++k) {
-      const int m2 = __ldg(c.g.nbr[0] + k);
-      if (m2 == c.u || m2 == c.v || !first_in_window(c, 0, k)) continue;
-      const uint32_t b = bloom_bit(m2);
-      atomicOr(&B.w[0][b >> 5], 1u << (b & 31));
-      const int idx = atomicAdd(&B.n2, 1);
-      if (idx < kB2Cap) B.list[idx] = m2;
-      else B.valid3 = 0;
+  int *lists[2] = {list0, list1};
+  for (int k = 2; k <= top && k - 2 < kBloomLayers; ++k) {
+    const int src = k & 1, dst = src ^ 1;  // layer k-1's list -> layer k's list
+    const int nsrc = k == 2 ? c.wui.len() : min(B.n[src], kBloomList);
+    bool over = false;
+    for (int i = lane; i < nsrc; i += 32) {
+      int m1;
+      if (k == 2) {
+        const int2 sl = slot_np(c, 0, c.wui.a + i);
+        m1 = sl.x;
+        if (m1 == c.u || m1 == c.v || !first_of(c, sl)) continue;
+      } else {
+        m1 = lists[src][i];
+      }
+      const Win w = window(c, 0, m1);
+      for (int q = w.a; q < w.b; ++q) {
+        const int2 s2 = slot_np(c, 0, q);
+        const int m2 = s2.x;
+        if (m2 == c.u || m2 == c.v || !first_of(c, s2)) continue;
+        const uint32_t b = bloom_bit(m2);
+        atomicOr(&B.w[k - 2][b >> 5], 1u << (b & 31));
+        const int idx = atomicAdd(&B.n[dst], 1);
+        if (idx < kBloomList) lists[dst][idx] = m2;
+        else over = true;
+      }
     }
-  }
-  __syncwarp();
-  const int n2 = min(B.n2, kB2Cap);
-  for (int i = lane; i < n2; i += 32) {
-    const Win w = window(c, 0, B.list[i]);
-    for (int k = w.a; k < w.b; ++k) {
-      const int m3 = __ldg(c.g.nbr[0] + k);
-      if (m3 == c.u || m3 == c.v || !first_in_window(c, 0, k)) continue;
-      const uint32_t b = bloom_bit(m3);
-      atomicOr(&B.w[1][b >> 5], 1u << (b & 31));
+    over = __any_sync(0xffffffffu, over);
+    __syncwarp();
+    if (lane == 0) {
+      B.valid |= 1 << (k - 2);  // B_k itself is complete (its bits are all set)
+      B.n[src] = 0;             // the list just consumed becomes the next output
     }
+    __syncwarp();
+    if (over) break;  // B_k's member list is incomplete: no deeper layer
   }
-  __syncwarp();
 }
 
 // Task kinds (one warp per task):
@@ -821,12 +837,15 @@ __device__ void build_bloom(const Ctx &c, TaskBloom &B, int lane) {
 // Each kind feeds ONE call site of the item / chain code below.
 __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
-    long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q) {
+    long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q,
+    int32_t *__restrict__ bloom_lists) {
   const int n = min(*in.count, in.cap);
   const int warps = gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   __shared__ TaskBloom blooms[kTaskThreads / 32];
   TaskBloom &bloom = blooms[threadIdx.x >> 5];
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int *blist0 = bloom_lists + (size_t)gwarp * 2 * kBloomList, *blist1 = blist0 + kBloomList;
   for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
     const Task t = in.q[i];
     if (t.row < 0) continue;
@@ -839,7 +858,8 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     Queue next = next_q;
     const bool chains = t.level != kLvlDomU && !(t.level == kLvlDomV && !(t.pad0 & kVCyc));
     if (chains && gr.cyc.maxd >= 2 && c.u != c.v && c.wui.len() > 0) {
-      build_bloom(c, bloom, lane);
+      // layers up to the one a depth-1 node needs for the deepest close
+      build_bloom(c, bloom, lane, 1 + gr.cyc.maxd, blist0, blist1);
       next.bloom = &bloom;
     }
     long long *orow = out + (int64_t)t.row * P.n;
@@ -870,7 +890,10 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
         }
         if (redo) {
           bool ok = false;
-          if (lane == 0) ok = emit(next, t.row, t.grp, kLvlDomV, t.path[0], -1, -1, -1, -1, t.a, t.b, redo);
+          // with filters built, a moderate window is walked here rather than
+          // rebuilding the filters in every domain task; wide ones are split
+          if (lane == 0 && !(next.bloom && (redo & kVCyc) && t.b - t.a <= kInPlace))
+            ok = emit(next, t.row, t.grp, kLvlDomV, t.path[0], -1, -1, -1, -1, t.a, t.b, redo);
           if (!__shfl_sync(0xffffffffu, ok, 0)) {  // queue full: this warp walks the declined parts too
             if (cand) {
               for (int j = t.a + lane; j < t.b; j += 32) {
@@ -911,8 +934,10 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
           cand = use;
         } else {
           bool ok = false;
-          if (lane == 0) ok = emit(next, t.row, t.grp, L, path[0], path[1], path[2], path[3], path[4], t.a, t.b);
-          if (__shfl_sync(0xffffffffu, ok, 0)) ja = jb = 0;  // split into chain tasks for the next round
+          if (lane == 0 && !(next.bloom && t.b - t.a <= kInPlace))
+            ok = emit(next, t.row, t.grp, L, path[0], path[1], path[2], path[3], path[4], t.a, t.b);
+          // split into chain tasks for the next round, or (filters built) walk the window here
+          if (__shfl_sync(0xffffffffu, ok, 0)) ja = jb = 0;
         }
       }
       for (int k = ja + lane; k < jb; k += 32)  // one entry per lane per step
@@ -1160,11 +1185,14 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     for (int i = 0; i < kHostPieces; ++i)
       TM_CUDA(cudaEventCreateWithFlags(&g->piece_ev[i], cudaEventDisableTiming));
   }
+  const int task_grid = 148 * (2048 / kTaskThreads);
+  if ((rc = g->bloom_lists.ensure_pooled(sizeof(int32_t) * 2 * kBloomList * (size_t)task_grid * (kTaskThreads / 32),
+                                         s, g->stream)))
+    return rc;
   if ((rc = g->split_counts.ensure_pooled(sizeof(int32_t) * kHostPieces, s, g->stream))) return rc;
   int32_t *piece_split = g->split_counts.as<int32_t>();
   g->prof_pending = g->prof;
   if (g->prof) TM_CUDA(cudaEventRecord(g->ev[0], s));
-  const int task_grid = 148 * (2048 / kTaskThreads);
   const int64_t per = (rows + pieces - 1) / pieces;
   for (int pc = 0; pc < pieces; ++pc) {
     const int64_t r0 = std::min<int64_t>(rows, pc * per), r1 = std::min<int64_t>(rows, r0 + per);
@@ -1186,7 +1214,8 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     for (int r = 0; r < rounds; ++r) {
       TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int32_t), s));
       k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po,
-                                                      g->split_scratch.as<int32_t>(), a, b);
+                                                      g->split_scratch.as<int32_t>(), a, b,
+                                                      g->bloom_lists.as<int32_t>());
       TM_LAUNCHED("k_mine_tasks");
       std::swap(a, b);
     }
