@@ -49,6 +49,7 @@ def args_parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--pieces", type=int, default=4, help="N > 1: pipelined all-gather pieces")
     return p.parse_args()
 
 
@@ -231,6 +232,12 @@ def main():
     E = g0.edge_count
     chunk = (E + world - 1) // world
     lo, hi = min(rank * chunk, E), min((rank + 1) * chunk, E)
+    # N > 1: interleaved pieces, each piece's all-gather overlaps the next
+    # piece's mining (distributed.piece_bounds)
+    from paper_2604_12241_b200.distributed import piece_bounds
+    pieces = a.pieces if world > 1 else 1
+    P, sub, pbounds = piece_bounds(E, world, pieces)
+    rows_local = sum(h - l for l, h in pbounds[rank]) if world > 1 else hi - lo
 
     t0 = time.perf_counter()
     g = tmb.DeviceGraph(g0.src, g0.dst, g0.time, node_count=g0.node_count, device=dev)
@@ -246,7 +253,8 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     out_local = torch.empty((chunk, C), dtype=torch.int64, device="cuda")
-    out_full = torch.empty((chunk * world, C), dtype=torch.int64, device="cuda") if world > 1 else None
+    out_pieces = torch.zeros((pieces, sub, C), dtype=torch.int64, device="cuda") if world > 1 else None
+    out_full = torch.empty((pieces * P, C), dtype=torch.int64, device="cuda") if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     _lib.check(_lib.load().tm_set_profiling(g.handle, 1), "tm_set_profiling")
 
@@ -265,10 +273,21 @@ def main():
         evm = torch.cuda.Event(enable_timing=True)
         c0 = _lib.kernel_launch_count()
         ev0.record(stream)
-        tmb.mine_rows_device(g, descs, lo, hi, out_local.data_ptr(), stream.cuda_stream)
-        evm.record(stream)  # mining done; the all-gather follows
-        if world > 1:
-            dist.all_gather_into_tensor(out_full, out_local)
+        if world == 1:
+            tmb.mine_rows_device(g, descs, lo, hi, out_local.data_ptr(), stream.cuda_stream)
+            evm.record(stream)
+        else:
+            works = []
+            for p in range(pieces):
+                plo, phi = pbounds[rank][p]
+                if phi > plo:
+                    tmb.mine_rows_device(g, descs, plo, phi, out_pieces[p].data_ptr(), stream.cuda_stream)
+                # NCCL waits for this stream, then gathers while the next piece is mined
+                works.append(dist.all_gather_into_tensor(out_full[p * P:(p + 1) * P], out_pieces[p],
+                                                         async_op=True))
+            evm.record(stream)  # all pieces mined (gathers may still run)
+            for w in works:
+                w.wait()
         ev1.record(stream)
         ev1.synchronize()
         st = tmb.last_stats(g)
@@ -292,7 +311,7 @@ def main():
     # roofline of the dominant kernel (compulsory-bytes model)
     peak, peak_src = peaks()
     b_edge = 16 + 24 + 8 * C + 8 * (g0.node_count + 1) / E
-    rows = hi - lo
+    rows = rows_local
     lm, hm = float(np.mean(light_ms)), float(np.mean(heavy_ms))
     dom_name, dom_ms = ("k_mine_warp", lm) if lm >= hm else ("k_mine_tasks+finalize", hm)
     achieved = rows * b_edge / (dom_ms / 1e3) / 1e9
@@ -316,7 +335,7 @@ def main():
     if not a.no_e2e:
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).pin_memory().numpy()
         hs, hd, ht = pin(g0.src), pin(g0.dst), pin(g0.time)
-        hout = torch.empty((rows, C), dtype=torch.int64).pin_memory().numpy()
+        hout = torch.empty((hi - lo, C), dtype=torch.int64).pin_memory().numpy()
         e2e_ms = []
         n_e2e = max(1, min(a.steps, 5))
         for step in range(2 + n_e2e):  # two untimed warm-up builds (pool, pinned pages)
@@ -360,7 +379,8 @@ def main():
             "data": "synthetic (reference synth model: power-law sources, uniform dst/time, planted "
                     "instances; edge ids time-ordered)",
             "config": dict(workload_config(a.config, cfg, g0, C),
-                           parallelism=f"edge-range x{world} + NCCL all-gather" if world > 1 else "1 GPU",
+                           parallelism=(f"edge ranges x{world}, {pieces} interleaved pieces, NCCL all-gather "
+                                        f"per piece overlapped with mining" if world > 1 else "1 GPU"),
                            graph_build_s=build_s, graph_device_gib=info.device_bytes / 2**30),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks,

@@ -54,6 +54,49 @@ def mine_sharded(n_edges: int, n_cols: int, rank: int, world: int,
     return gather_rows(local, n_edges, group)
 
 
+def piece_bounds(n_edges: int, world: int, pieces: int) -> tuple[int, int, list[list[tuple[int, int]]]]:
+    """Interleaved piece assignment for a pipelined gather.
+
+    The trigger range is cut into `pieces` global pieces of P rows (P a
+    multiple of `world`); rank r mines sub-range r of every piece.  The
+    all-gather of piece p then lands exactly on global rows [p*P, (p+1)*P)
+    in order, so each piece's gather can start while the next piece is
+    mined — no reordering pass.  Returns (P, sub = P // world,
+    bounds[rank][piece] = (lo, hi)), ranges clamped to n_edges."""
+    if world < 1 or pieces < 1:
+        raise ValueError("world and pieces must be >= 1")
+    sub = (n_edges + world * pieces - 1) // (world * pieces) if n_edges else 0
+    P = sub * world
+    bounds = [[(min(p * P + r * sub, n_edges), min(p * P + (r + 1) * sub, n_edges)) for p in range(pieces)]
+              for r in range(world)]
+    return P, sub, bounds
+
+
+def mine_pipelined(n_edges: int, n_cols: int, rank: int, world: int,
+                   mine_block: Callable[[int, int, object], None], pieces: int = 4, device="cuda", group=None):
+    """Like mine_sharded, but the gather of each piece is issued (async) as
+    soon as the piece is mined, so it overlaps the next piece's mining."""
+    import torch
+    import torch.distributed as dist
+    P, sub, bounds = piece_bounds(n_edges, world, pieces)
+    full = torch.empty((pieces * P, n_cols), dtype=torch.int64, device=device)
+    local = torch.zeros((pieces, sub, n_cols), dtype=torch.int64, device=device)
+    nccl = dist.get_backend(group) == "nccl"
+    works = []
+    for p in range(pieces):
+        lo, hi = bounds[rank][p]
+        if hi > lo:
+            mine_block(lo, hi, local[p])
+        dst = full[p * P:(p + 1) * P]
+        if nccl:
+            works.append(dist.all_gather_into_tensor(dst, local[p], group=group, async_op=True))
+        else:  # gloo (CPU tests): list form
+            works.append(dist.all_gather(list(dst.split(sub)), local[p], group=group, async_op=True))
+    for w in works:
+        w.wait()
+    return full[:n_edges]
+
+
 def mine_distributed(graph, plans, *, group=None):
     """`mine` across the ranks of the default (NCCL) process group.
 
@@ -78,8 +121,8 @@ def mine_distributed(graph, plans, *, group=None):
         mine_rows_device(dg, descs, lo, hi, out.data_ptr(), side.cuda_stream)
         torch.cuda.current_stream().wait_stream(side)
 
-    full = mine_sharded(dg.edge_count, len(descs), dist.get_rank(group), dist.get_world_size(group),
-                        block, device="cuda", group=group)
+    full = mine_pipelined(dg.edge_count, len(descs), dist.get_rank(group), dist.get_world_size(group),
+                          block, device="cuda", group=group)
     values = full.cpu().numpy()
     return FeatureMatrix(tuple(p.name for p in plans), values, graph.edge_src, graph.edge_dst,
                          graph.edge_time, getattr(graph, "edge_label", dg.edge_label))

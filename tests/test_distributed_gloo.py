@@ -14,7 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2604_12241_b200.distributed import mine_sharded, partition
+from paper_2604_12241_b200.distributed import mine_pipelined, mine_sharded, partition, piece_bounds
 
 
 def test_partition_equal_chunks():
@@ -25,6 +25,18 @@ def test_partition_equal_chunks():
     assert partition(0, 2) == (0, [(0, 0), (0, 0)])
     with pytest.raises(ValueError):
         partition(5, 0)
+
+
+def test_piece_bounds_cover_rows_in_order():
+    for n, world, pieces in ((1001, 2, 4), (10, 3, 2), (4, 2, 4), (0, 2, 3), (7, 4, 1)):
+        P, sub, b = piece_bounds(n, world, pieces)
+        assert P == sub * world
+        rows = []
+        for p in range(pieces):  # gathered piece p = rank 0's part, rank 1's part, ...
+            for r in range(world):
+                lo, hi = b[r][p]
+                rows.extend(range(lo, hi))
+        assert rows == list(range(n))
 
 
 def _free_port() -> int:
@@ -44,6 +56,8 @@ def _worker(rank, world, port, src, dst, t, names, delta, q):
         out[: hi - lo] = torch.from_numpy(og.mine(cols, lo, hi, threads=2))
 
     full = mine_sharded(len(src), len(cols), rank, world, block, device="cpu")
+    piped = mine_pipelined(len(src), len(cols), rank, world, block, pieces=3, device="cpu")
+    assert torch.equal(full, piped)
     q.put((rank, full.numpy().copy()))
     dist.barrier()
     dist.destroy_process_group()
