@@ -306,7 +306,7 @@ __device__ __forceinline__ bool pull_candidates(const Ctx &c, const CycGroup &cg
                                                 const Win &w, int *use, int &ja, int &jb) {
   const int nu = useful_nodes(c.g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, maxd, J, use);
   if (nu < 0 || nu * 4 > w.len()) return false;
-  TM_CNT(kCtrVSkip, 1);
+  TM_CNT(kCtrPull, 1);
   ja = 0;
   jb = nu;
   return true;

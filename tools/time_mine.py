@@ -1,4 +1,5 @@
-"""Launch-list timing of one full mine call (GPU box): python tools/time_own.py LIB [config]"""
+"""Device time of one full mine call (all 14 columns, device output), CUDA events on the launch
+stream (GPU box): python tools/time_mine.py LIB [config]"""
 import os, sys
 sys.path.insert(0, ".")
 os.environ["TM_LIB"] = os.path.abspath(sys.argv[1])
