@@ -396,3 +396,30 @@ def test_instances_vs_reference(tmb):
         assert got.shape == want.shape and np.array_equal(got, want), f"{m['name']} d={m['delta']}"
         total += len(recs)
     assert total > 1000
+
+
+def test_host_output_pieces_match_device_output(tmb):
+    """Pinned host output of >= 1 M rows is mined in 8 pieces whose D2H
+    overlaps the next piece (tm_mine): same values as the device-output
+    path, and sampled rows equal the oracle."""
+    import torch
+    from paper_2604_12241_b200 import synth
+    cfg = synth.SynthConfig(60000, 1_200_000, 6 * 86400, seed=31, powerlaw_exponent=1.1,
+                            plants=(synth.PlantSpec("cycle_4", 30), synth.PlantSpec("sg_count", 30)))
+    g0 = synth.generate(cfg)
+    g = tmb.DeviceGraph(g0.src, g0.dst, g0.time, node_count=g0.node_count)
+    descs = [tmb.lower_plan(p) for p in tmb.full_pattern_set(86400)]
+    E, C = g.edge_count, len(descs)
+    assert E >= 1 << 20
+    pinned = torch.empty((E, C), dtype=torch.int64).pin_memory().numpy()
+    tmb.mine_rows(g, descs, 0, E, out=pinned)
+    dev = torch.empty((E, C), dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    tmb.mine_rows_device(g, descs, 0, E, dev.data_ptr(), s.cuda_stream)
+    s.synchronize()
+    assert np.array_equal(pinned, dev.cpu().numpy())
+    og = OracleGraph(g0.src, g0.dst, g0.time)
+    names = list(tmb.FULL_PATTERN_SET)
+    for lo in (0, E // 3, E - 700):
+        want = og.mine([column(n, 86400) for n in names], lo, lo + 700)
+        assert np.array_equal(pinned[lo:lo + 700], want), lo
