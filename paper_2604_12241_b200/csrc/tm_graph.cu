@@ -294,6 +294,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
   TM_CUDA(cudaStreamSynchronize(s));
   if (h1.bad) return fail(TM_E_BAD_ARG, std::to_string(h1.bad) + " edge endpoint(s) outside [0, n_nodes)");
   g->n_selfloops = (int64_t)h1.selfloops;
+  g->t_span = (int64_t)((unsigned long long)h1.tmax - (unsigned long long)h1.tmin);
 
   // 2. narrow ids, time keys
   DevBuf ka, kb, va, vb;

@@ -75,6 +75,7 @@ struct CycGroup {
   int32_t k[kMaxCyc];      // min_size per entry
   int8_t depth[kMaxCyc];
   int8_t col[kMaxCyc];     // output column per entry
+  int32_t deep_split;      // chain nodes with wider windows leave the warp kernel (pull tasks)
 };
 
 // the columns sharing one delta: one set of trigger windows, one
@@ -187,6 +188,7 @@ struct tm_graph {
   cudaStream_t stream = nullptr;
   bool owns_stream = false;
   int64_t n_nodes = 0, n_edges = 0, n_ranks = 0, n_selfloops = 0;
+  int64_t t_span = 0;  // max - min timestamp (ticks)
   int64_t max_deg[2] = {0, 0};
   int rank_bits = 0, node_bits = 0;
   int64_t device_bytes = 0;

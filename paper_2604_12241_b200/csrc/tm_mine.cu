@@ -52,8 +52,14 @@ namespace {
 constexpr int kThreads = TM_WARP_THREADS;  // k_mine_warp block
 constexpr int kWarps = kThreads / 32;
 constexpr int kTaskThreads = 256;
-constexpr int kDomSplit = 256;       // a trigger slice above this becomes domain tasks
-constexpr int kDeepSplit = 64;       // chain nodes with wider windows become chain tasks
+#ifndef TM_DOM_SPLIT
+#define TM_DOM_SPLIT 128  // swept 64..512 with TM_DEEP_SPLIT 4..128
+#endif
+#ifndef TM_DEEP_SPLIT
+#define TM_DEEP_SPLIT 8  // short windows (mean in-window degree <= 2); long ones use 64
+#endif
+constexpr int kDomSplit = TM_DOM_SPLIT;    // a trigger slice above this becomes domain tasks
+constexpr int kDeepSplit = TM_DEEP_SPLIT;  // CycGroup::deep_split for short windows
 constexpr int kTaskSpan = 128;       // entries per task (4 per lane)
 constexpr int kLvlDomU = 8, kLvlDomV = 9;  // Task::level of domain tasks
 constexpr int kLvlPullV = 10;  // Task::level: gs + cycles of a hub v expanded from u's side
@@ -96,6 +102,7 @@ constexpr int kBloomLayers = 4;    // B_2 .. B_5
 constexpr int kBloomWords = 256;   // 8192 bits per layer
 constexpr int kBloomList = 4096;   // members of one layer kept to build the next (global scratch)
 constexpr int kInPlace = 4096;     // a filtered pull task walks windows up to this long itself
+constexpr int kBloomMin = 64;      // tasks over narrower windows do not build filters
 struct TaskBloom {
   uint32_t w[kBloomLayers][kBloomWords];
   int32_t valid;  // bit k-2: layer B_k complete
@@ -333,7 +340,7 @@ __device__ __forceinline__ void chain_pick(const Ctx &c, const CycGroup &cg, int
     int ja = w.a, jb = w.b;
     const int *cand = nullptr;
     int use[kBCap];
-    if (w.len() > kDeepSplit) {
+    if (w.len() > cg.deep_split) {
       if constexpr (PI) {
         if (pull_candidates(c, cg, MAXD, L + 2, w, use, ja, jb)) cand = use;
         else if (emit(qu, row, grp, L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b)) return;
@@ -398,7 +405,7 @@ __device__ __forceinline__ void cycles_a1(const Ctx &c, const CycGroup &cg, int 
   int ja = w.a, jb = w.b;
   const int *cand = nullptr;
   int use[kBCap];
-  if (w.len() > kDeepSplit) {
+  if (w.len() > cg.deep_split) {
     if constexpr (PI) {
       if (pull_candidates(c, cg, MAXD, 2, w, use, ja, jb)) cand = use;
       else if (emit(qu, row, grp, 1, path[0], -1, -1, -1, -1, w.a, w.b)) return;
@@ -857,7 +864,8 @@ __global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
     // chain walks of this task get the trigger's backward-layer filters
     Queue next = next_q;
     const bool chains = t.level != kLvlDomU && !(t.level == kLvlDomV && !(t.pad0 & kVCyc));
-    if (chains && gr.cyc.maxd >= 2 && c.u != c.v && c.wui.len() > 0) {
+    // (narrow windows are cheaper to walk than the filters are to build)
+    if (chains && gr.cyc.maxd >= 2 && c.u != c.v && c.wui.len() > 0 && t.b - t.a > kBloomMin) {
       // layers up to the one a depth-1 node needs for the deepest close
       build_bloom(c, bloom, lane, 1 + gr.cyc.maxd, blist0, blist1);
       next.bloom = &bloom;
@@ -1134,6 +1142,15 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
       k_own_windows<<<grid_for(E, 256), 256, 0, s>>>(dg, dp.gr[k].lo_tab, dir, lo, hi, tab);
       TM_LAUNCHED("k_own_windows");
       dp.gr[k].own[dir] = tab;
+    }
+    // Hand-off width for chain nodes: with short windows (mean windowed
+    // degree <= 2) backward pruning in the task kernel wins for any node
+    // wider than kDeepSplit; with long windows nearly every node is that
+    // wide and the per-task overhead dominates, so only hubs (> 64) leave.
+    {
+      const double mean_w = (double)g->n_edges / (double)std::max<int64_t>(g->n_nodes, 1) *
+                            (double)deltas[k] / (double)std::max<int64_t>(g->t_span, 1);
+      dp.gr[k].cyc.deep_split = mean_w <= 2.0 ? kDeepSplit : 64;
     }
     // task rounds: domain tasks, then one per chain level below a1
     if (dp.gr[k].udom || dp.gr[k].vdom)
