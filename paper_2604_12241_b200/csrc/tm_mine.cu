@@ -51,7 +51,13 @@ namespace {
 #endif
 constexpr int kThreads = TM_WARP_THREADS;  // k_mine_warp block
 constexpr int kWarps = kThreads / 32;
-constexpr int kTaskThreads = 256;
+#ifndef TM_TASK_THREADS
+#define TM_TASK_THREADS 256
+#endif
+#ifndef TM_TASK_MINB
+#define TM_TASK_MINB 4
+#endif
+constexpr int kTaskThreads = TM_TASK_THREADS;
 #ifndef TM_DOM_SPLIT
 #define TM_DOM_SPLIT 128  // swept 64..512 with TM_DEEP_SPLIT 4..128
 #endif
@@ -842,7 +848,7 @@ __device__ void build_bloom(const Ctx &c, TaskBloom &B, int lane, int top, int *
 //                         nodes, or chain tasks for the next round
 //   level 1..4            a piece of a chain node's window
 // Each kind feeds ONE call site of the item / chain code below.
-__global__ void __launch_bounds__(kTaskThreads, 4) k_mine_tasks(
+__global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q,
     int32_t *__restrict__ bloom_lists) {
