@@ -3,14 +3,22 @@
 
 One step = one pass of the mining stage over every trigger edge of the
 workload graph (all 14 feature columns for all E edges), graph resident in
-HBM, output int64 (E, 14) in HBM; for N > 1 the edge range is split into N
-equal chunks (one per rank) and the columns are assembled on every GPU by one
-NCCL all-gather.  `value` = E / max-over-ranks step time.
+HBM, output int64 (E, 14) in HBM; for N > 1 the edge range is cut into
+interleaved pieces (one sub-range per rank per piece) whose NCCL all-gathers
+overlap the next piece's mining.  `value` = E / max-over-ranks
+step time.  Default workload: the north-star HI-Large shape
+(BASELINE.json:north_star, ~180 M transactions) on 1 B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config hi-small]
+After the timed steps the GPU output is checked against the CPU oracle
+(oracle/tm_oracle.c, pinned to the reference's own outputs) on >= 1024
+random 1000-trigger blocks of the same graph — the reference's _mine_range
+seam (engine.py:607-646); the oracle's time on those blocks is the
+cpu_baseline.  Any mismatch: the JSON line still prints, exit status 1.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config hi-large]
     python bench.py --impl reference ...   # CPU oracle port on the host cores
 
-Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement.
+Prints ONE JSON line (rank 0).  See DESIGN.md §6.
 """
 
 from __future__ import annotations
@@ -20,6 +28,7 @@ import json
 import os
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 from pathlib import Path
@@ -33,6 +42,14 @@ METRIC = "transactions mined/sec, full pattern set, 1/2/4/8 B200; % HBM roofline
 UNIT = "edges/s"
 DELTA = 86400
 FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback, GB/s
+# per-family breakdown (report per-family fractions)
+FAMILIES = {
+    "streaming": ["fan_in", "fan_out", "deg_in_src", "deg_out_src", "deg_in_dst", "deg_out_dst", "cycle_2"],
+    "cycles_3_6": ["cycle_3", "cycle_4", "cycle_5", "cycle_6"],
+    "sg": ["sg_count"],
+    "gs": ["gs_count"],
+    "stack": ["stack_count"],
+}
 
 
 def log(*a):
@@ -44,16 +61,20 @@ def args_parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="hi-small", choices=["cfg1", "hi-small", "hi-medium", "hi-large"])
+    p.add_argument("--config", default="hi-large", choices=["cfg1", "hi-small", "hi-medium", "hi-large"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
-    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget (s)")
+    p.add_argument("--parity-blocks", type=int, default=1024, help="sampled 1000-trigger blocks checked")
+    p.add_argument("--no-parity", action="store_true", help="skip the oracle check (and cpu_baseline)")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--no-families", action="store_true")
     p.add_argument("--pieces", type=int, default=4, help="N > 1: pipelined all-gather pieces")
+    p.add_argument("--wide", action="store_true", help="N > 1: int64 transport (default int32 + flags)")
     return p.parse_args()
 
 
-def workload(name: str):
+def generate(name: str):
     from paper_2604_12241_b200 import synth
     cfg = synth.CONFIGS[name]
     t0 = time.perf_counter()
@@ -63,8 +84,43 @@ def workload(name: str):
     return cfg, g
 
 
-def workload_config(name, cfg, g, n_cols):
-    return {"workload": name, "n_nodes": int(g.node_count), "n_edges": int(g.edge_count),
+class Workload:
+    """Edge arrays of the synthetic graph (what every rank's replica is built from)."""
+
+    def __init__(self, cfg, src, dst, time_, node_count):
+        self.cfg, self.src, self.dst, self.time, self.node_count = cfg, src, dst, time_, node_count
+        self.edge_count = len(src)
+
+
+def workload(name: str, rank: int = 0, world: int = 1, dist=None) -> Workload:
+    """Generate once: with N > 1 rank 0 generates and the other ranks map its
+    arrays (no per-rank 180 M-edge regeneration)."""
+    from paper_2604_12241_b200 import synth
+    if world == 1:
+        cfg, g = generate(name)
+        return Workload(cfg, g.src, g.dst, g.time, g.node_count)
+    tag = f"tmb_{name}_{os.environ.get('MASTER_PORT', '0')}"
+    base = Path(tempfile.gettempdir())
+    if rank == 0:
+        cfg, g = generate(name)
+        for k in ("src", "dst", "time"):
+            np.save(base / f"{tag}_{k}.npy", getattr(g, k))
+    dist.barrier()
+    arr = {k: np.load(base / f"{tag}_{k}.npy", mmap_mode="r") for k in ("src", "dst", "time")}
+    cfg = synth.CONFIGS[name]
+    n = int(max(arr["src"].max(), arr["dst"].max())) + 1
+    w = Workload(cfg, np.ascontiguousarray(arr["src"]), np.ascontiguousarray(arr["dst"]),
+                 np.ascontiguousarray(arr["time"]), max(n, cfg.node_count))
+    dist.barrier()
+    if rank == 0:
+        for k in ("src", "dst", "time"):
+            (base / f"{tag}_{k}.npy").unlink(missing_ok=True)
+    return w
+
+
+def workload_config(name, w: Workload, n_cols):
+    cfg = w.cfg
+    return {"workload": name, "n_nodes": int(w.node_count), "n_edges": int(w.edge_count),
             "columns": n_cols, "delta": DELTA, "powerlaw_alpha": cfg.powerlaw_exponent,
             "horizon_ticks": cfg.time_horizon, "seed": cfg.seed, "edge_order": "time-ordered",
             "pattern_set": "fan_in/out, deg x4, cycle_2..6, sg_count, gs_count, stack_count",
@@ -77,6 +133,22 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def bytes_per_edge(n_cols: int, n_nodes: int, n_edges: int) -> float:
+    """SURVEY §8d compulsory bytes per trigger: 16 (src, dst, t) + 24 (one
+    out + one in CSR entry) + 8 C (features) + 8 (N + 1) / E (indptr)."""
+    return 16 + 24 + 8 * n_cols + 8 * (n_nodes + 1) / max(n_edges, 1)
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -136,65 +208,82 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline / reference arm: the oracle port (oracle/tm_oracle.c), which
-# restates the reference's per-trigger algorithm, on all host threads
+# the CPU oracle (oracle/tm_oracle.c): parity checker, cpu_baseline and the
+# reference arm — never on the measured GPU path
 
 
 _ORACLE = {}
 
 
-def cpu_sample(g, names, budget_s: float, seed: int = 0):
-    """Time the oracle on random contiguous 1000-trigger blocks until the
-    budget is spent.  Returns (edges_per_s, rows, seconds, blocks, build_s);
-    the CPU graph build is done once and not timed."""
-    from oracle.oracle import OracleGraph, column
+def oracle_graph(w: Workload):
+    from oracle.oracle import OracleGraph
     t0 = time.perf_counter()
-    if id(g) not in _ORACLE:
-        _ORACLE[id(g)] = OracleGraph(g.src, g.dst, g.time, node_count=g.node_count)
-    og = _ORACLE[id(g)]
-    build_s = time.perf_counter() - t0
-    cols = [column(n, DELTA) for n in names]
+    if id(w) not in _ORACLE:
+        _ORACLE[id(w)] = OracleGraph(w.src, w.dst, w.time, node_count=w.node_count)
+    return _ORACLE[id(w)], time.perf_counter() - t0
+
+
+def sample_blocks(n_edges: int, n_blocks: int, seed: int, size: int = 1000) -> list[tuple[int, int]]:
     rng = np.random.default_rng(seed)
-    rows = blocks = 0
-    spent = 0.0
-    threads = os.cpu_count() or 1
-    while spent < budget_s and blocks < 4096:
-        lo = int(rng.integers(0, max(1, g.edge_count - 1000)))
-        hi = min(lo + 1000, g.edge_count)
+    out = []
+    for _ in range(n_blocks):
+        lo = int(rng.integers(0, max(1, n_edges - size)))
+        out.append((lo, min(lo + size, n_edges)))
+    return out
+
+
+def oracle_blocks(w: Workload, names, blocks, threads: int):
+    """Oracle rows of each block, and the seconds spent mining them."""
+    from oracle.oracle import column
+    og, _ = oracle_graph(w)
+    cols = [column(n, DELTA) for n in names]
+    res, spent = [], 0.0
+    for lo, hi in blocks:
         t = time.perf_counter()
-        og.mine(cols, lo, hi, threads=threads)
+        res.append(og.mine(cols, lo, hi, threads=threads))
         spent += time.perf_counter() - t
-        rows += hi - lo
-        blocks += 1
-    return rows / spent, rows, spent, blocks, build_s
+    return res, spent
 
 
 def run_reference(a):
+    """--impl reference: the reference's CPU algorithm (the pinned C port, on
+    all host threads) on the same workload; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import paper_2604_12241_b200 as tmb
-    cfg, g = workload(a.config)
+    w = workload(a.config)
     names = list(tmb.FULL_PATTERN_SET)
-    per_step = max(2.0, min(10.0, 150.0 / max(1, a.steps + a.warmup)))
+    og, build_s = oracle_graph(w)
+    threads = os.cpu_count() or 1
+    per_step = max(2.0, min(6.0, 90.0 / max(1, a.steps + a.warmup)))
     vals = []
     for step in range(a.warmup + a.steps):
-        v, rows, spent, blocks, build_s = cpu_sample(g, names, per_step, seed=step)
+        blocks, rows, spent, k = [], 0, 0.0, 0
+        while spent < per_step:
+            bl = sample_blocks(w.edge_count, 16, seed=1000 * step + k)
+            k += 1
+            _, s = oracle_blocks(w, names, bl, threads)
+            spent += s
+            rows += sum(h - l for l, h in bl)
+            blocks += bl
         if step >= a.warmup:
-            vals.append((v, rows, spent, blocks))
+            vals.append((rows / spent, rows, spent, len(blocks)))
     value = float(np.mean([v for v, *_ in vals]))
-    ms = float(np.mean([s / r * g.edge_count * 1e3 for _, r, s, _ in vals]))
-    cores = os.cpu_count() or 1
+    ms = float(np.mean([s / r * w.edge_count * 1e3 for _, r, s, _ in vals]))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (reference synth model)",
-        "config": workload_config(a.config, cfg, g, len(names)),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "config": workload_config(a.config, w, len(names)),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "cpu": cpu_model(),
                          "sample": f"per step: random contiguous 1000-trigger blocks of the {a.config} "
-                                   f"graph, all 14 columns, ~{per_step:.0f}s of CPU work; "
-                                   f"ms_per_step extrapolated to all {g.edge_count} triggers"},
+                                   f"graph, all 14 columns, ~{per_step:.0f}s of CPU work on {threads} threads "
+                                   f"(oracle/tm_oracle.c, the reference's algorithm restated in C and pinned "
+                                   f"to its outputs); ms_per_step extrapolated to all {w.edge_count} triggers; "
+                                   f"CPU graph build {build_s:.1f}s untimed"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -202,6 +291,36 @@ def run_reference(a):
 
 
 # ---------------------------------------------------------------------------
+
+
+def timed_mine(tmb, g, descs, lo, hi, out, stream, flush, steps, warmup, sampler_dev=None):
+    """CUDA-event times (ms) of `steps` full mining calls after `warmup`, L2
+    flushed before each; returns (step_ms, warp_kernel_ms, launches, clocks)."""
+    import torch
+    from paper_2604_12241_b200 import _lib
+    step_ms, light_ms = [], []
+    launches = 0
+    sampler = None
+    for step in range(warmup + steps):
+        timed = step >= warmup
+        if timed and step == warmup:
+            torch.cuda.synchronize()
+            if sampler_dev is not None:
+                sampler = ClockSampler(sampler_dev)
+        flush.zero_()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0 = _lib.kernel_launch_count()
+        ev0.record(stream)
+        tmb.mine_rows_device(g, descs, lo, hi, out.data_ptr(), stream.cuda_stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        st = tmb.last_stats(g)
+        if timed:
+            launches += _lib.kernel_launch_count() - c0
+            step_ms.append(ev0.elapsed_time(ev1))
+            light_ms.append(st.light_ms)
+    clocks = sampler.stop() if sampler else None
+    return step_ms, light_ms, launches, clocks
 
 
 def main():
@@ -224,152 +343,223 @@ def main():
 
     import paper_2604_12241_b200 as tmb
     from paper_2604_12241_b200 import _lib
+    from paper_2604_12241_b200.distributed import INT32_MAX, piece_bounds
 
-    cfg, g0 = workload(a.config)
+    w = workload(a.config, rank, world, dist if world > 1 else None)
     plans = tmb.full_pattern_set(DELTA)
     plans, descs = tmb.lower_all(plans)
+    names = [p.name for p in plans]
     C = len(descs)
-    E = g0.edge_count
-    chunk = (E + world - 1) // world
-    lo, hi = min(rank * chunk, E), min((rank + 1) * chunk, E)
-    # N > 1: interleaved pieces, each piece's all-gather overlaps the next
-    # piece's mining (distributed.piece_bounds)
-    from paper_2604_12241_b200.distributed import piece_bounds
+    E = w.edge_count
     pieces = a.pieces if world > 1 else 1
     P, sub, pbounds = piece_bounds(E, world, pieces)
-    rows_local = sum(h - l for l, h in pbounds[rank]) if world > 1 else hi - lo
+    narrow = world > 1 and not a.wide
 
     t0 = time.perf_counter()
-    g = tmb.DeviceGraph(g0.src, g0.dst, g0.time, node_count=g0.node_count, device=dev)
+    g = tmb.DeviceGraph(w.src, w.dst, w.time, node_count=w.node_count, device=dev)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     info = g.info()
     log(f"[bench] rank {rank}: graph built in {build_s:.2f}s, {info.device_bytes / 2**30:.2f} GiB, "
-        f"max out/in degree {info.max_out_degree}/{info.max_in_degree}, rows [{lo},{hi})")
+        f"max out/in degree {info.max_out_degree}/{info.max_in_degree}")
 
     # a non-default stream: its handle is non-NULL, so the library launches on
     # it (NULL would select the graph's own stream) and the events below see
     # exactly the mining kernels' stream
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    out_local = torch.empty((chunk, C), dtype=torch.int64, device="cuda")
-    out_pieces = torch.zeros((pieces, sub, C), dtype=torch.int64, device="cuda") if world > 1 else None
-    out_full = torch.empty((pieces * P, C), dtype=torch.int64, device="cuda") if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     _lib.check(_lib.load().tm_set_profiling(g.handle, 1), "tm_set_profiling")
 
-    step_ms, light_ms, heavy_ms, heavy_n, mine_ms = [], [], [], [], []
-    launches = 0
-    clocks = None
-    for step in range(a.warmup + a.steps):
-        timed = step >= a.warmup
-        if timed and step == a.warmup:
-            if world > 1:
+    if world == 1:
+        out = torch.empty((E, C), dtype=torch.int64, device="cuda")
+        step_ms, light_ms, launches, clocks = timed_mine(tmb, g, descs, 0, E, out, stream, flush, a.steps,
+                                                         a.warmup, sampler_dev=dev)
+        total_ms = compute_ms = float(np.sum(step_ms))
+        full_out = out
+    else:
+        out_pieces = torch.zeros((pieces, sub, C), dtype=torch.int64, device="cuda")
+        out_full = torch.empty((pieces * P, C), dtype=torch.int64, device="cuda")
+        if narrow:
+            n32 = torch.empty((pieces, sub, C), dtype=torch.int32, device="cuda")
+            f32 = torch.empty((pieces * P, C), dtype=torch.int32, device="cuda")
+            flags = torch.zeros((pieces, 1), dtype=torch.int32, device="cuda")
+            flags_all = torch.empty((world, pieces), dtype=torch.int32, device="cuda")
+        step_ms, light_ms, mine_ms = [], [], []
+        launches = 0
+        sampler = None
+        for step in range(a.warmup + a.steps):
+            timed = step >= a.warmup
+            if timed and step == a.warmup:
                 dist.barrier()
-            torch.cuda.synchronize()
-            sampler = ClockSampler(dev)
-        flush.zero_()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        evm = torch.cuda.Event(enable_timing=True)
-        c0 = _lib.kernel_launch_count()
-        ev0.record(stream)
-        if world == 1:
-            tmb.mine_rows_device(g, descs, lo, hi, out_local.data_ptr(), stream.cuda_stream)
-            evm.record(stream)
-        else:
+                torch.cuda.synchronize()
+                sampler = ClockSampler(dev)
+            flush.zero_()
+            ev0, ev1, evm = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            c0 = _lib.kernel_launch_count()
+            ev0.record(stream)
             works = []
             for p in range(pieces):
                 plo, phi = pbounds[rank][p]
                 if phi > plo:
                     tmb.mine_rows_device(g, descs, plo, phi, out_pieces[p].data_ptr(), stream.cuda_stream)
-                # NCCL waits for this stream, then gathers while the next piece is mined
-                works.append(dist.all_gather_into_tensor(out_full[p * P:(p + 1) * P], out_pieces[p],
-                                                         async_op=True))
+                dst = out_full[p * P:(p + 1) * P]
+                if narrow:  # int32 transport, overflow flag per piece (distributed.py)
+                    flags[p, 0] = (out_pieces[p].max() > INT32_MAX).to(torch.int32)
+                    n32[p].copy_(out_pieces[p])
+                    works.append(dist.all_gather_into_tensor(f32[p * P:(p + 1) * P], n32[p], async_op=True))
+                else:  # NCCL waits for this stream, then gathers while the next piece is mined
+                    works.append(dist.all_gather_into_tensor(dst, out_pieces[p], async_op=True))
             evm.record(stream)  # all pieces mined (gathers may still run)
-            for w in works:
-                w.wait()
-        ev1.record(stream)
-        ev1.synchronize()
-        st = tmb.last_stats(g)
-        if timed:
-            launches += _lib.kernel_launch_count() - c0
-            step_ms.append(ev0.elapsed_time(ev1))
-            mine_ms.append(ev0.elapsed_time(evm))
-            light_ms.append(st.light_ms)
-            heavy_ms.append(st.heavy_ms)
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    total_ms = float(np.sum(step_ms))
-    compute_ms = float(np.sum(mine_ms))
-    if world > 1:
-        t = torch.tensor([total_ms, compute_ms], dtype=torch.float64, device="cuda")
+            for wk in works:
+                wk.wait()
+            if narrow:
+                dist.all_gather_into_tensor(flags_all.view(-1), flags.view(-1))
+                bad = flags_all.amax(dim=0).cpu().numpy()
+                for p in range(pieces):
+                    dst = out_full[p * P:(p + 1) * P]
+                    if bad[p]:
+                        dist.all_gather_into_tensor(dst, out_pieces[p])
+                    else:
+                        dst.copy_(f32[p * P:(p + 1) * P])
+            ev1.record(stream)
+            ev1.synchronize()
+            st = tmb.last_stats(g)
+            if timed:
+                launches += _lib.kernel_launch_count() - c0
+                step_ms.append(ev0.elapsed_time(ev1))
+                mine_ms.append(ev0.elapsed_time(evm))
+                light_ms.append(st.light_ms)
+        torch.cuda.synchronize()
+        clocks = sampler.stop()
+        t = torch.tensor([float(np.sum(step_ms)), float(np.sum(mine_ms))], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, compute_ms = float(t[0].item()), float(t[1].item())
+        full_out = out_full[:E]
     ms_per_step = total_ms / a.steps
     value = E / (ms_per_step / 1e3)
 
-    # roofline of the dominant kernel (compulsory-bytes model)
+    # roofline (compulsory-bytes model): the whole mining step
+    # is the unit — every kernel of the step (window tables, k_mine_warp, task
+    # rounds) is charged, none is credited with another's bytes
     peak, peak_src = peaks()
-    b_edge = 16 + 24 + 8 * C + 8 * (g0.node_count + 1) / E
-    rows = rows_local
-    lm, hm = float(np.mean(light_ms)), float(np.mean(heavy_ms))
-    dom_name, dom_ms = ("k_mine_warp", lm) if lm >= hm else ("k_mine_tasks+finalize", hm)
-    achieved = rows * b_edge / (dom_ms / 1e3) / 1e9
+    b_edge = bytes_per_edge(C, w.node_count, E)
+    lm = float(np.mean(light_ms))
+    step_alone_ms = compute_ms / a.steps  # mining only (N > 1: gathers excluded)
+    achieved = E / world * b_edge / (step_alone_ms / 1e3) / 1e9 if world > 1 else E * b_edge / (ms_per_step / 1e3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
-        tj = json.loads(tfile.read_text())
-        ent = tj.get(a.config, {}).get(dom_name)
-        if ent:
-            traffic = ent.get("dram_bytes")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
-                "kernel_ms": dom_ms, "warp_kernel_ms": lm, "task_kernels_ms": hm,
+        ent = json.loads(tfile.read_text()).get(a.config, {})
+        if ent.get("step_dram_bytes"):
+            traffic = ent["step_dram_bytes"]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "mining step (k_own_windows + k_mine_warp + task rounds)",
+                "step_ms": step_alone_ms, "warp_kernel_ms": lm,
+                "warp_kernel_share": lm / step_alone_ms if step_alone_ms > 0 else None,
                 "bytes_per_edge": b_edge, "peak_source": peak_src,
-                "step_frac": E * b_edge / (ms_per_step / 1e3) / 1e9 / peak,
+                "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum "
+                                  "summed over the step's kernels (ncu --set full, one step)",
                 "model": "compulsory bytes per trigger = 16 (src,dst,t) + 24 (one out + one in CSR "
-                         "entry) + 8*C (features) + 8(N+1)/E (indptr), SURVEY.md §8d"}
+                         "entry) + 8*C (features) + 8(N+1)/E (indptr), SURVEY.md §8d; E x B / step time"}
 
-    # end-to-end through the public API: pinned host arrays -> build -> mine -> host
+    # per-family fractions, 1 GPU: each family mined alone
+    families = None
+    if world == 1 and not a.no_families:
+        families = {}
+        for fam, cols in FAMILIES.items():
+            fdescs = [d for d, n in zip(descs, names) if n in cols]
+            fout = torch.empty((E, len(fdescs)), dtype=torch.int64, device="cuda")
+            fms, flm, _, _ = timed_mine(tmb, g, fdescs, 0, E, fout, stream, flush, max(3, a.steps // 2), 2)
+            del fout
+            fb = bytes_per_edge(len(fdescs), w.node_count, E)
+            fstep = float(np.mean(fms))
+            families[fam] = {"columns": cols, "ms_per_step": fstep, "edges_per_s": E / (fstep / 1e3),
+                             "warp_kernel_ms": float(np.mean(flm)), "bytes_per_edge": fb,
+                             "frac": E * fb / (fstep / 1e3) / 1e9 / peak}
+            log(f"[bench] family {fam}: {fstep:.2f} ms, frac {families[fam]['frac']:.3f}")
+        torch.cuda.synchronize()
+
+    # parity on sampled blocks + the CPU baseline on the same blocks (rank 0)
+    parity = cpu = None
+    if rank == 0 and not a.no_parity:
+        threads = os.cpu_count() or 1
+        og, build_cpu = oracle_graph(w)
+        blocks = sample_blocks(E, a.parity_blocks, seed=2604)
+        want, spent = oracle_blocks(w, names, blocks, threads)
+        # keep sampling for the CPU baseline until its budget is spent
+        extra = 0
+        while world == 1 and spent < a.cpu_seconds:
+            more = sample_blocks(E, 64, seed=9000 + extra)
+            extra += 1
+            rws, s = oracle_blocks(w, names, more, threads)
+            blocks += more
+            want += rws
+            spent += s
+        # only the sampled rows come back to the host
+        idx = torch.from_numpy(np.concatenate([np.arange(lo, hi) for lo, hi in blocks])).to(full_out.device)
+        got = full_out.index_select(0, idx).cpu().numpy()
+        bad_rows = 0
+        bad_cols = set()
+        at = 0
+        for (lo, hi), wv in zip(blocks, want):
+            diff = got[at:at + hi - lo] != wv
+            at += hi - lo
+            if diff.any():
+                bad_rows += int(diff.any(axis=1).sum())
+                bad_cols.update(names[j] for j in np.nonzero(diff.any(axis=0))[0])
+        rows = sum(h - l for l, h in blocks)
+        parity = {"blocks": len(blocks), "rows": rows, "mismatches": bad_rows, "bad_columns": sorted(bad_cols),
+                  "checker": "oracle/tm_oracle.c (CPU restatement pinned to the reference's outputs, "
+                             "tests/test_oracle_golden.py) on random 1000-trigger blocks, all columns, "
+                             "bit-exact int64"}
+        if world == 1:
+            cpu = {"value": rows / spent, "unit": UNIT, "cores": threads, "kind": "port", "cpu": cpu_model(),
+                   "sample": f"{len(blocks)} random contiguous 1000-trigger blocks ({rows} triggers) of the "
+                             f"same graph, all {C} columns, {spent:.1f}s on {threads} threads; "
+                             f"oracle/tm_oracle.c (CPU graph build {build_cpu:.1f}s untimed)"}
+        log(f"[bench] parity: {bad_rows} mismatching rows of {rows} ({len(blocks)} blocks)")
+
+    # end to end through the drop-in API: pinned host edge arrays -> mine()
+    # (H2D + GPU CSR build + mining + D2H into the pinned FeatureMatrix)
     e2e = None
     if not a.no_e2e:
+        from types import SimpleNamespace
+
+        from paper_2604_12241_b200.distributed import mine_distributed
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).pin_memory().numpy()
-        hs, hd, ht = pin(g0.src), pin(g0.dst), pin(g0.time)
-        hout = torch.empty((hi - lo, C), dtype=torch.int64).pin_memory().numpy()
+        hs, hd, ht = pin(w.src), pin(w.dst), pin(w.time)
+        lab = np.full(E, -1, dtype=np.int8)
         e2e_ms = []
-        n_e2e = max(1, min(a.steps, 5))
-        for step in range(2 + n_e2e):  # two untimed warm-up builds (pool, pinned pages)
+        for step in range(2 + a.e2e_steps):  # two untimed warm-up calls (pool, pinned pages)
             if world > 1:
                 dist.barrier()
+            # a fresh graph object every step: mine() uploads and builds it
+            host_graph = SimpleNamespace(edge_src=hs, edge_dst=hd, edge_time=ht, node_count=w.node_count,
+                                         edge_label=lab)
             t = time.perf_counter()
-            ge = tmb.DeviceGraph(hs, hd, ht, node_count=g0.node_count, device=dev)
-            tmb.mine_rows(ge, descs, lo, hi, out=hout)
+            if world == 1:
+                fm = tmb.mine(host_graph, plans)
+            else:
+                fm = mine_distributed(host_graph, plans, pieces=pieces, narrow=narrow)
             dt = (time.perf_counter() - t) * 1e3
-            ge.free()
+            fm.device_graph.free()
+            del fm, host_graph
             if step >= 2:
                 e2e_ms.append(dt)
-        em = float(np.mean(e2e_ms))
+        em, med = float(np.mean(e2e_ms)), float(np.median(e2e_ms))
         if world > 1:
-            t = torch.tensor([em], dtype=torch.float64, device="cuda")
+            t = torch.tensor([em, med], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            em = float(t.item())
+            em, med = float(t[0].item()), float(t[1].item())
         e2e = {"value": E / (em / 1e3), "unit": UNIT, "h2d_bytes_per_step": 24 * E * world,
-               "d2h_bytes_per_step": 8 * E * C, "ms_per_step": em,
-               "step_ms": [round(x, 3) for x in e2e_ms], "median_ms": float(np.median(e2e_ms)),
+               "d2h_bytes_per_step": 8 * E * C * world, "ms_per_step": em, "median_ms": med,
+               "median_value": E / (med / 1e3), "max_over_median": float(np.max(e2e_ms)) / med,
+               "step_ms": [round(x, 3) for x in e2e_ms],
+               "api": "paper_2604_12241_b200.mine(graph, plans)" if world == 1 else
+                      "paper_2604_12241_b200.distributed.mine_distributed(graph, plans)",
                "includes": "H2D of src/dst/time (pinned), GPU CSR build, mining, D2H of the int64 "
-                           "feature block (pinned)"}
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        try:
-            names = [p.name for p in plans]
-            v, r, s, blocks, build_cpu = cpu_sample(g0, names, a.cpu_seconds)
-            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-                   "sample": f"{blocks} random contiguous 1000-trigger blocks ({r} triggers) of the "
-                             f"same graph, all {C} columns, {s:.1f}s; oracle/tm_oracle.c on "
-                             f"{os.cpu_count()} threads (CPU graph build {build_cpu:.1f}s untimed)"}
-        except Exception as exc:  # reported, never substituted for the GPU number
-            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-                   "sample": f"failed: {exc}"}
+                           "feature block into the FeatureMatrix (pinned host pool)"}
 
     if rank == 0:
         line = {
@@ -378,11 +568,12 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (reference synth model: power-law sources, uniform dst/time, planted "
                     "instances; edge ids time-ordered)",
-            "config": dict(workload_config(a.config, cfg, g0, C),
+            "config": dict(workload_config(a.config, w, C),
                            parallelism=(f"edge ranges x{world}, {pieces} interleaved pieces, NCCL all-gather "
-                                        f"per piece overlapped with mining" if world > 1 else "1 GPU"),
+                                        f"({'int32 + overflow flags' if narrow else 'int64'}) per piece "
+                                        f"overlapped with mining" if world > 1 else "1 GPU"),
                            graph_build_s=build_s, graph_device_gib=info.device_bytes / 2**30),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "families": families, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks,
             # scaling with and without the feature all-gather
             "compute_only": {"value": E / (compute_ms / a.steps / 1e3), "unit": UNIT,
@@ -393,6 +584,8 @@ def main():
     g.free()
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and parity["mismatches"]:
+        return 1
     return 0
 
 

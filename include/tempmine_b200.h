@@ -36,9 +36,13 @@
  * Conventions: C linkage, fixed-width integers, no torch types.  Every call
  * returns TM_OK (0) or a negative tm_status; tm_last_error() then holds a
  * thread-local message.  Host buffers are caller-owned; device memory is
- * owned by the tm_graph handle.  Calls on one graph must be serialized by
- * the caller (the Python wrapper does this).  There is no CPU fallback: a
- * plan the GPU path does not implement fails with TM_E_UNSUPPORTED_PLAN.
+ * owned by the tm_graph handle.  Calls on one graph must not run
+ * concurrently from several host threads (they share the handle's scratch
+ * and result buffers): the Python wrapper holds a per-graph lock around
+ * every call sequence (DeviceGraph.lock).  Work a call enqueues on a user
+ * stream is ordered before the next call on the same graph and before
+ * tm_graph_free.  There is no CPU fallback: a plan the GPU path does not
+ * implement fails with TM_E_UNSUPPORTED_PLAN.
  */
 #ifndef TEMPMINE_B200_H
 #define TEMPMINE_B200_H
@@ -49,7 +53,7 @@
 extern "C" {
 #endif
 
-#define TM_ABI_VERSION 4
+#define TM_ABI_VERSION 5
 
 /* pattern families (plan.py kernel hints + the extended north-star set) */
 enum tm_family {
@@ -102,14 +106,14 @@ typedef struct tm_graph_info {
 
 typedef struct tm_mine_stats {
   int64_t triggers;       /* rows mined by the last tm_mine */
-  int64_t heavy_triggers; /* rows deferred to the cooperative (warp) kernel,
-                             -1 when not read back (device-output calls) */
+  int64_t heavy_triggers; /* rows whose slices went to the task queue (split
+                             rows), -1 when not read back (device-output calls) */
   int64_t kernel_launches;/* launches issued by the last tm_mine */
-  float light_ms;         /* CUDA-event time of the last call's per-thread
-                             kernel (profiling on), else -1 */
-  float heavy_ms;         /* same for the heavy (per-warp + task) kernels,
-                             summed over pipeline chunks (they overlap the
-                             next chunk's light kernel) */
+  float light_ms;         /* CUDA-event time (profiling on, else -1) of the
+                             trigger kernel (k_mine_warp), after the call's
+                             window tables */
+  float heavy_ms;         /* from there to the end of the task rounds and
+                             k_mine_finalize (task kernel time) */
   float total_ms;         /* CUDA-event time of the whole call on the device */
   int32_t reserved;
 } tm_mine_stats;
@@ -351,6 +355,12 @@ int tm_set_profiling(tm_graph *g, int on);
 
 /* Total kernels this process launched through the library. */
 int64_t tm_kernel_launch_count(void);
+
+/* Page-locked (pinned, portable) host memory: outputs written here get the
+ * overlapped piece-wise D2H of tm_mine.  Replaces the pageable np.zeros the
+ * reference's mine() allocates for FeatureMatrix.values (engine.py:693). */
+int tm_host_alloc(int64_t bytes, void **out);
+void tm_host_free(void *p);
 
 const char *tm_last_error(void);
 

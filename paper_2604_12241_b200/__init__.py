@@ -10,7 +10,7 @@ ExecutionPlans or the structurally identical ones `builtin_plan` builds.
 from ._lib import TempmineError, UnsupportedPlanError, kernel_launch_count
 from .engine import (EngineInvariantError, FeatureMatrix, InstanceRecord, collect_instance_records,
                      last_stats, lower_all, merge_features, mine,
-                     mine_members, mine_rows, mine_rows_device, order_plans,
+                     mine_members, mine_members_device, mine_rows, mine_rows_device, order_plans,
                      write_instances)
 from .graph import DeviceGraph, GraphStats, as_device_graph
 from .plan import (BUILTIN_COLUMNS, EXTENDED_COLUMNS, FULL_PATTERN_SET, ExecutionPlan, PlanDesc,
@@ -21,7 +21,7 @@ __all__ = [
     "ExecutionPlan", "FeatureMatrix", "InstanceRecord", "collect_instance_records", "GraphStats", "PlanDesc", "TempmineError",
     "UnsupportedPlanError", "as_device_graph", "builtin_plan", "canonical_shape", "full_pattern_set",
     "kernel_launch_count", "last_stats", "load_builtin", "lower_all", "lower_plan", "merge_features",
-    "mine", "mine_members", "mine_rows", "mine_rows_device", "order_plans", "recognize", "write_instances",
+    "mine", "mine_members", "mine_members_device", "mine_rows", "mine_rows_device", "order_plans", "recognize", "write_instances",
 ]
 
 __version__ = "0.1.0"

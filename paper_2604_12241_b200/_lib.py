@@ -131,10 +131,19 @@ SIGNATURES = {
     "tm_ingest_free": (None, [_P]),
     "tm_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
     "tm_kernel_launch_count": (ctypes.c_int64, []),
+    "tm_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(_P)]),
+    "tm_host_free": (None, [_P]),
     "tm_last_error": (ctypes.c_char_p, []),
     "tm_graph_free": (None, [_P]),
 }
-ABI_VERSION = 4
+ABI_VERSION = 5
+
+# work counters of -DTM_COUNTERS=1 builds (tm_debug_counters; order of
+# dev::CtrId in csrc/tm_device.cuh)
+COUNTER_NAMES = ["trig", "u_walk", "u_item", "v_walk", "v_item", "window", "bisect32", "scan_call",
+                 "scan_load", "pair_call", "bisect64", "inner_call", "inner_walk", "chain1", "chain2",
+                 "chain3", "chain4", "close_call", "close_walk", "dom_task", "chain_task", "first",
+                 "inner_skip", "pulls", "queue_full", "slot_full", "useful_over", "bloom_over"]
 
 
 class TempmineError(RuntimeError):

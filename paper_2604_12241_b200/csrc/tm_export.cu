@@ -140,7 +140,7 @@ int scan64(unsigned long long *a, int64_t n, cudaStream_t s) {
     return TM_OK;
   }
   unsigned long long *sums = nullptr;
-  TM_CUDA(cudaMallocAsync(&sums, sizeof(unsigned long long) * tiles, s));
+  TM_CUDA(pool_malloc((void **)&sums, sizeof(unsigned long long) * tiles, s));
   k_scan64<<<(unsigned)tiles, kST, 0, s>>>(a, n, sums);
   TM_LAUNCHED("k_scan64");
   int rc = scan64(sums, tiles, s);

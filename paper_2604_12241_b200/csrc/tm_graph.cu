@@ -164,7 +164,7 @@ __global__ void k_gather_time(const uint32_t *__restrict__ rnk, const int64_t *_
 int DevBuf::ensure_on(size_t n, cudaStream_t s) {
   if (n <= bytes && p) return TM_OK;
   release();
-  cudaError_t e = cudaMallocAsync(&p, n ? n : 16, s);
+  cudaError_t e = pool_malloc(&p, n ? n : 16, s);
   if (e != cudaSuccess) {
     p = nullptr;
     cudaGetLastError();
@@ -181,10 +181,13 @@ int DevBuf::ensure_on(size_t n, cudaStream_t s) {
 int DevBuf::ensure_pooled(size_t n, cudaStream_t s, cudaStream_t free_stream) {
   if (n <= bytes && p) return TM_OK;
   if (p) {
-    cudaDeviceSynchronize();  // earlier calls on other streams may still use the old block
+    // the old block may still be read by this call's earlier kernels on s
+    // or (tm_graph::begin makes s wait for them) by earlier calls
+    cudaStreamSynchronize(s);
+    cudaStreamSynchronize(free_stream);
     release();
   }
-  cudaError_t e = cudaMallocAsync(&p, n ? n : 16, s);
+  cudaError_t e = pool_malloc(&p, n ? n : 16, s);
   if (e != cudaSuccess) {
     p = nullptr;
     cudaGetLastError();
@@ -395,14 +398,6 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
   TM_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(TM_E_BAD_ARG, "bad device ordinal");
   TM_CUDA(cudaSetDevice(device));
-  {  // keep freed pool memory cached: rebuilding a graph then costs no cudaMalloc
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaGetLastError();
-  }
   tm_graph *g = new tm_graph();
   g->device = device;
   g->n_nodes = n_nodes;
@@ -520,7 +515,13 @@ extern "C" int tm_graph_export_csr(const tm_graph *g, int dir, int64_t *indptr, 
 extern "C" void tm_graph_free(tm_graph *g) {
   if (!g) return;
   cudaSetDevice(g->device);
-  cudaDeviceSynchronize();  // kernels on user streams may still read the graph
+  // kernels enqueued on user streams may still read the graph: the last
+  // call's completion event covers them (tm_graph::end)
+  if (g->done_ev) {
+    cudaEventSynchronize(g->done_ev);
+    cudaEventDestroy(g->done_ev);
+  }
+  cudaStreamSynchronize(g->stream);
   bool own = g->owns_stream;
   cudaStream_t s = g->stream;
   for (int i = 0; i < 3; ++i)

@@ -359,7 +359,9 @@ extern "C" int tm_collect_instances(tm_graph *g, const tm_plan_desc *plans, int 
   }
   const int64_t R = g->n_ranks;
   int rc;
-  if ((rc = g->lo_tabs.ensure(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups))) return rc;
+  TM_CUDA(g->begin(s));
+  if ((rc = g->lo_tabs.ensure_pooled(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups, s, g->stream)))
+    return rc;
   for (int k = 0; k < dp.ngroups; ++k) {
     dp.gr[k].lo_tab = g->lo_tabs.as<uint32_t>() + (size_t)k * R;
     k_lo_table_i<<<grid_for(R, 256), 256, 0, s>>>(g->uniq_time.as<int64_t>(), R, deltas[k],

@@ -114,6 +114,10 @@ void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);
 int cuda_fail(cudaError_t e, const char *what);
 void count_launch(int n = 1);
+// the library's stream-ordered memory pool on `device` (tm_api.cu) and an
+// allocation from it on stream s (current device)
+cudaMemPool_t lib_pool(int device);
+cudaError_t pool_malloc(void **p, size_t n, cudaStream_t s);
 // in-place exclusive scan of n uint64 on stream s (tm_export.cu)
 int scan_u64_exclusive(unsigned long long *a, int64_t n, cudaStream_t s);
 
@@ -214,6 +218,19 @@ struct tm_graph {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t piece_ev[8] = {};
   tmb::DevBuf split_counts;
+  // completion of the last call that enqueued work on a (possibly user)
+  // stream: the next call's stream waits on it before touching the shared
+  // scratch, and tm_graph_free waits on it before freeing
+  cudaEvent_t done_ev = nullptr;
+
+  cudaError_t begin(cudaStream_t s) { return done_ev ? cudaStreamWaitEvent(s, done_ev, 0) : cudaSuccess; }
+  cudaError_t end(cudaStream_t s) {
+    if (!done_ev) {
+      cudaError_t e = cudaEventCreateWithFlags(&done_ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaEventRecord(done_ev, s);
+  }
 
   tmb::DevGraph dev() const;
 };

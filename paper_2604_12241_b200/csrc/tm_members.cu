@@ -366,6 +366,7 @@ extern "C" int tm_mine_members(tm_graph *g, const tm_plan_desc *plans, int n_pla
   if (n_plans == 0 || E == 0) return TM_OK;
   TM_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  TM_CUDA(g->begin(s));  // the shared scratch below may still be in use by the previous call
   const int64_t launches0 = tm_kernel_launch_count();
   DevPlans dp{};
   dp.n = n_plans;
@@ -382,7 +383,8 @@ extern "C" int tm_mine_members(tm_graph *g, const tm_plan_desc *plans, int n_pla
   }
   const int64_t R = g->n_ranks;
   int rc;
-  if ((rc = g->lo_tabs.ensure(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups))) return rc;
+  if ((rc = g->lo_tabs.ensure_pooled(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups, s, g->stream)))
+    return rc;
   for (int k = 0; k < dp.ngroups; ++k) {
     dp.gr[k].lo_tab = g->lo_tabs.as<uint32_t>() + (size_t)k * R;
     k_lo_table_m<<<grid_for(R, 256), 256, 0, s>>>(g->uniq_time.as<int64_t>(), R, deltas[k],
@@ -394,7 +396,7 @@ extern "C" int tm_mine_members(tm_graph *g, const tm_plan_desc *plans, int n_pla
   if (out_on_device) {
     d_out = reinterpret_cast<long long *>(out);  // accumulated into
   } else {
-    if ((rc = g->out_scratch.ensure(bytes))) return rc;
+    if ((rc = g->out_scratch.ensure_pooled(bytes, s, g->stream))) return rc;
     d_out = g->out_scratch.as<long long>();
     TM_CUDA(cudaMemsetAsync(d_out, 0, bytes, s));
   }
@@ -406,6 +408,7 @@ extern "C" int tm_mine_members(tm_graph *g, const tm_plan_desc *plans, int n_pla
     TM_CUDA(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, s));
     TM_CUDA(cudaStreamSynchronize(s));
   }
+  TM_CUDA(g->end(s));
   g->last.kernel_launches = tm_kernel_launch_count() - launches0;
   return TM_OK;
 }

@@ -106,7 +106,10 @@ struct Queue {
 // stays exact; a layer that could not be built completely is "all".
 constexpr int kBloomLayers = 4;    // B_2 .. B_5
 constexpr int kBloomWords = 256;   // 8192 bits per layer
-constexpr int kBloomList = 4096;   // members of one layer kept to build the next (global scratch)
+#ifndef TM_BLOOM_LIST
+#define TM_BLOOM_LIST 4096
+#endif
+constexpr int kBloomList = TM_BLOOM_LIST;  // members of one layer kept to build the next (global scratch)
 constexpr int kInPlace = 4096;     // a filtered pull task walks windows up to this long itself
 constexpr int kBloomMin = 64;      // tasks over narrower windows do not build filters
 struct TaskBloom {
@@ -120,15 +123,28 @@ __device__ __forceinline__ bool bloom_has(const uint32_t *w, int x) {
   return (w[b >> 5] >> (b & 31)) & 1u;
 }
 
+// reserve n slots of the queue, or none: the count never passes the
+// capacity (a plain atomicAdd past a full queue could wrap the int32 count
+// on hub windows and turn later reservations into out-of-bounds writes)
+__device__ __forceinline__ int reserve(const Queue &qu, int n) {
+  int cur = *(volatile int32_t *)qu.count;
+  while (true) {
+    if (cur > qu.cap - n) return -1;
+    const int seen = atomicCAS(qu.count, cur, cur + n);
+    if (seen == cur) return cur;
+    cur = seen;
+  }
+}
+
 // cut [a, b) into kTaskSpan pieces; false (caller walks it itself) when the
 // queue is full — the walk is slower but exact and still on the GPU
 __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p1, int p2, int p3,
                      int p4, int a, int b, int parts = kVAll) {
   const int n = (b - a + kTaskSpan - 1) / kTaskSpan;
   TM_CNT(level >= kLvlDomU ? kCtrDomTask : kCtrChainTask, n);
-  const int base = atomicAdd(qu.count, n);
-  if (base + n > qu.cap) {
-    for (int k = base; k < qu.cap; ++k) qu.q[k].row = -1;  // holes stay empty
+  const int base = reserve(qu, n);
+  if (base < 0) {
+    TM_CNT(kCtrQueueFull, 1);
     return false;
   }
   for (int k = 0; k < n; ++k) {
@@ -149,9 +165,12 @@ __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p
 // one task for the whole range [a, b) (a pull task): false when the queue is full
 __device__ bool emit_whole(const Queue &qu, int row, int grp, int level, const int (&path)[kMaxChain],
                            int a, int b) {
-  const int k = atomicAdd(qu.count, 1);
   TM_CNT(kCtrChainTask, 1);
-  if (k >= qu.cap) return false;
+  const int k = reserve(qu, 1);
+  if (k < 0) {
+    TM_CNT(kCtrQueueFull, 1);
+    return false;
+  }
   Task t;
   t.row = row;
   t.grp = (int8_t)grp;
@@ -260,7 +279,10 @@ __device__ __forceinline__ void close_at(const CycGroup &cg, int d, int cc, CycA
 // `cand[ja..jb)` of useful nodes (see useful_nodes), each probed for
 // a_L -> a.  Every level has ONE call site of the next, so the inlined
 // template tree stays linear in the depth.
-constexpr int kBCap = 48;
+#ifndef TM_BCAP
+#define TM_BCAP 48  // tests build a tiny-cap variant to exercise the overflow paths
+#endif
+constexpr int kBCap = TM_BCAP;
 
 // Backward sets: every chain that contributes reaches u inside the window,
 // so a node at depth j closing at depth d >= j lies in B_{2+d-j}, where
@@ -288,17 +310,17 @@ __device__ __noinline__ int useful_nodes(const DevGraph &g, int u, int v, uint32
   for (int j = wa; j < wb; ++j) {  // B_1
     const int m = __ldg(g.nbr[0] + j);
     if (m == u || m == v || !first_in_window(c, 0, j)) continue;
-    if (!bset_add(node, 0, n, m)) return -1;
+    if (!bset_add(node, 0, n, m)) return TM_CNT(kCtrUsefulOver, 1), -1;
   }
   lend[1] = n;
   for (int k = 2; k <= H; ++k) {
     for (int i = lend[k - 2]; i < lend[k - 1]; ++i) {
       const Win w = window(c, 0, node[i]);
-      if (w.len() > kBCap) return -1;
+      if (w.len() > kBCap) return TM_CNT(kCtrUsefulOver, 1), -1;
       for (int j = w.a; j < w.b; ++j) {
         const int m = __ldg(g.nbr[0] + j);
         if (m == u || m == v || !first_in_window(c, 0, j)) continue;
-        if (!bset_add(node, lend[k - 1], n, m)) return -1;
+        if (!bset_add(node, lend[k - 1], n, m)) return TM_CNT(kCtrUsefulOver, 1), -1;
       }
     }
     lend[k] = n;
@@ -308,7 +330,7 @@ __device__ __noinline__ int useful_nodes(const DevGraph &g, int u, int v, uint32
     if (!(mask & (1 << d))) continue;
     const int k = 2 + d - J;
     for (int i = lend[k - 1]; i < lend[k]; ++i)
-      if (!bset_add(use, 0, nu, node[i])) return -1;
+      if (!bset_add(use, 0, nu, node[i])) return TM_CNT(kCtrUsefulOver, 1), -1;
   }
   return nu;
 }
@@ -646,6 +668,7 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
         slot = atomicAdd(split_n, 1);
         if (slot >= split_cap) {
           slot = -2;  // no scratch left: the warp walks the slices itself
+          TM_CNT(kCtrSlotFull, 1);
         } else {
           split_rows[2 * slot] = (int)row;
           split_rows[2 * slot + 1] = gi;
@@ -824,7 +847,7 @@ __device__ void build_bloom(const Ctx &c, TaskBloom &B, int lane, int top, int *
         atomicOr(&B.w[k - 2][b >> 5], 1u << (b & 31));
         const int idx = atomicAdd(&B.n[dst], 1);
         if (idx < kBloomList) lists[dst][idx] = m2;
-        else over = true;
+        else over = true, TM_CNT(kCtrBloomOver, 1);
       }
     }
     over = __any_sync(0xffffffffu, over);
@@ -852,7 +875,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q,
     int32_t *__restrict__ bloom_lists) {
-  const int n = min(*in.count, in.cap);
+  const int n = min((unsigned)*in.count, (unsigned)in.cap);
   const int warps = gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   __shared__ TaskBloom blooms[kTaskThreads / 32];
@@ -1078,6 +1101,7 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   if (rows == 0 || n_plans == 0) return TM_OK;
   TM_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  TM_CUDA(g->begin(s));  // the shared scratch below may still be in use by the previous call
   const int64_t launches0 = tm_kernel_launch_count();
 
   // delta groups (one window set + one lower-bound table per distinct delta)
@@ -1170,8 +1194,16 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     if ((rc = g->out_scratch.ensure_pooled(sizeof(long long) * (size_t)rows * n_plans, s, g->stream))) return rc;
     d_out = g->out_scratch.as<long long>();
   }
+#ifdef TM_TASK_CAP  // tiny-cap test builds: queue-full / split-slot fallbacks
+  const int64_t task_cap = TM_TASK_CAP;
+#else
   const int64_t task_cap = std::min<int64_t>(std::max<int64_t>(1 << 18, rows / 8), 1 << 24);
+#endif
+#ifdef TM_SPLIT_CAP
+  const int64_t split_cap = TM_SPLIT_CAP;
+#else
   const int64_t split_cap = std::min<int64_t>(std::max<int64_t>(1 << 16, rows / 16), 1 << 22);
+#endif
   if ((rc = g->heavy_n.ensure_pooled(sizeof(int32_t) * 4, s, g->stream)) ||
       (rc = g->heavy_q.ensure_pooled(sizeof(int32_t) * 2 * (size_t)split_cap, s, g->stream)) ||
       (rc = g->split_scratch.ensure_pooled(sizeof(int32_t) * 3 * (size_t)split_cap, s, g->stream)) ||
@@ -1269,6 +1301,7 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   } else {
     g->last.heavy_triggers = -1;  // not read back on the async path
   }
+  TM_CUDA(g->end(s));
   g->last.kernel_launches = tm_kernel_launch_count() - launches0;
   return TM_OK;
 }

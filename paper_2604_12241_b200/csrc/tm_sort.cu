@@ -174,7 +174,7 @@ int exclusive_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, cudaStream_
     return TM_OK;
   }
   uint32_t *sums = nullptr;
-  TM_CUDA(cudaMallocAsync(&sums, sizeof(uint32_t) * tiles, s));
+  TM_CUDA(pool_malloc((void **)&sums, sizeof(uint32_t) * tiles, s));
   k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, sums);
   TM_LAUNCHED("k_scan_tiles");
   int rc = exclusive_scan_u32(sums, sums, tiles, s);
@@ -192,7 +192,7 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *v
   if (n <= 1 || nbits <= 0) return TM_OK;
   const int64_t ntiles = (n + kTile - 1) / kTile;
   uint32_t *counts = nullptr;
-  TM_CUDA(cudaMallocAsync(&counts, sizeof(uint32_t) * kRadix * ntiles, s));
+  TM_CUDA(pool_malloc((void **)&counts, sizeof(uint32_t) * kRadix * ntiles, s));
   uint64_t *ka = keys, *kb = ktmp;
   uint32_t *va = vals, *vb = vtmp;
   for (int shift = 0; shift < nbits; shift += 8) {

@@ -9,6 +9,18 @@ all_gather_into_tensor over NVLink / NVSwitch assembles the int64 (E, C)
 feature block on every GPU — the replacement of the reference's fork pool
 and host-side block merge (engine.py:677-699).  One process per GPU,
 torch.distributed for the plumbing.
+
+Members-attribution columns (engine.py:629-640) add into the rows of every
+member edge, not only the trigger's: each rank accumulates its triggers'
+contributions into a full (E, C) block and the blocks are summed with one
+all-reduce — the reference's merge_features sum (engine.py:106-120).
+
+Transport: counts are int64, but nearly every column of a real graph stays
+far below 2^31.  `narrow=True` gathers each piece as int32 plus a one-byte
+overflow flag per rank; a piece whose flag is set anywhere is gathered again
+as int64, so the assembled block is bit-exact either way while the common
+case moves half the bytes over NVLink (HI-Large, C = 14: 10.1 instead of
+20.2 GB).
 """
 
 from __future__ import annotations
@@ -16,6 +28,8 @@ from __future__ import annotations
 from typing import Callable
 
 import numpy as np
+
+INT32_MAX = 2**31 - 1
 
 
 def partition(n_edges: int, world: int) -> tuple[int, list[tuple[int, int]]]:
@@ -26,6 +40,15 @@ def partition(n_edges: int, world: int) -> tuple[int, list[tuple[int, int]]]:
     return chunk, [(min(r * chunk, n_edges), min((r + 1) * chunk, n_edges)) for r in range(world)]
 
 
+def _all_gather(dst, src, group, async_op=False):
+    """all_gather_into_tensor on NCCL; the list form on gloo (CPU tests)."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        return dist.all_gather_into_tensor(dst, src, group=group, async_op=async_op)
+    parts = list(dst.split(src.shape[0]))
+    return dist.all_gather(parts, src, group=group, async_op=async_op)
+
+
 def gather_rows(local, n_edges: int, group=None):
     """All-gather equal (chunk, C) blocks into (n_edges, C) on every rank."""
     import torch
@@ -33,11 +56,7 @@ def gather_rows(local, n_edges: int, group=None):
     world = dist.get_world_size(group)
     chunk, c = local.shape
     full = torch.empty((chunk * world, c), dtype=local.dtype, device=local.device)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(full, local, group=group)
-    else:  # gloo (CPU tests): list form
-        parts = list(full.split(chunk))
-        dist.all_gather(parts, local, group=group)
+    _all_gather(full, local, group)
     return full[:n_edges]
 
 
@@ -73,56 +92,116 @@ def piece_bounds(n_edges: int, world: int, pieces: int) -> tuple[int, int, list[
 
 
 def mine_pipelined(n_edges: int, n_cols: int, rank: int, world: int,
-                   mine_block: Callable[[int, int, object], None], pieces: int = 4, device="cuda", group=None):
+                   mine_block: Callable[[int, int, object], None], pieces: int = 4, device="cuda", group=None,
+                   narrow: bool = False, stats: dict | None = None):
     """Like mine_sharded, but the gather of each piece is issued (async) as
-    soon as the piece is mined, so it overlaps the next piece's mining."""
+    soon as the piece is mined, so it overlaps the next piece's mining.
+
+    narrow=True: int32 transport with per-piece overflow flags (module doc);
+    `stats` (if given) receives {"pieces_int64": n} — pieces that had to be
+    re-gathered at full width."""
     import torch
-    import torch.distributed as dist
     P, sub, bounds = piece_bounds(n_edges, world, pieces)
     full = torch.empty((pieces * P, n_cols), dtype=torch.int64, device=device)
     local = torch.zeros((pieces, sub, n_cols), dtype=torch.int64, device=device)
-    nccl = dist.get_backend(group) == "nccl"
     works = []
+    if narrow:
+        full32 = torch.empty((pieces * P, n_cols), dtype=torch.int32, device=device)
+        flags = torch.zeros((pieces, 1), dtype=torch.int32, device=device)
+        flags_all = torch.empty((world, pieces), dtype=torch.int32, device=device)
+        narrow_local = torch.empty((pieces, sub, n_cols), dtype=torch.int32, device=device)
     for p in range(pieces):
         lo, hi = bounds[rank][p]
         if hi > lo:
             mine_block(lo, hi, local[p])
-        dst = full[p * P:(p + 1) * P]
-        if nccl:
-            works.append(dist.all_gather_into_tensor(dst, local[p], group=group, async_op=True))
-        else:  # gloo (CPU tests): list form
-            works.append(dist.all_gather(list(dst.split(sub)), local[p], group=group, async_op=True))
+        if narrow:
+            # counts are >= 0: one max decides whether int32 holds the piece
+            if sub > 0:
+                flags[p, 0] = (local[p].max() > INT32_MAX).to(torch.int32)
+            narrow_local[p].copy_(local[p])  # wraps on overflow; the flag redoes the piece
+            works.append(_all_gather(full32[p * P:(p + 1) * P], narrow_local[p], group, async_op=True))
+        else:
+            works.append(_all_gather(full[p * P:(p + 1) * P], local[p], group, async_op=True))
     for w in works:
         w.wait()
+    if narrow:
+        _all_gather(flags_all.view(-1), flags.view(-1), group)  # rank r -> row r
+        bad = flags_all.amax(dim=0).cpu().numpy()
+        for p in range(pieces):
+            dst = full[p * P:(p + 1) * P]
+            if bad[p]:
+                _all_gather(dst, local[p], group)
+            else:
+                dst.copy_(full32[p * P:(p + 1) * P])
+        if stats is not None:
+            stats["pieces_int64"] = int(np.count_nonzero(bad))
     return full[:n_edges]
 
 
-def mine_distributed(graph, plans, *, group=None):
+def sum_members(n_edges: int, n_cols: int, rank: int, world: int,
+                mine_range: Callable[[int, int, object], None], device="cuda", group=None):
+    """Members attribution across ranks: `mine_range(lo, hi, acc)` ADDS the
+    contributions of triggers [lo, hi) into the full (n_edges, C) block acc;
+    rank r takes chunk r of the trigger range and one all-reduce(SUM)
+    combines the blocks (engine.py:106-120 merge by sum)."""
+    import torch
+    import torch.distributed as dist
+    _, bounds = partition(n_edges, world)
+    lo, hi = bounds[rank]
+    acc = torch.zeros((n_edges, n_cols), dtype=torch.int64, device=device)
+    if hi > lo:
+        mine_range(lo, hi, acc)
+    dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    return acc
+
+
+def mine_distributed(graph, plans, *, group=None, pieces: int = 4, narrow: bool = True):
     """`mine` across the ranks of the default (NCCL) process group.
 
     Each rank builds its own device replica of `graph` on
     torch.cuda.current_device(); returns the FeatureMatrix on every rank.
+    Trigger-attribution columns: pipelined all-gather (≤ 32 columns per
+    launch, as `mine`); members-attribution columns: all-reduce of full
+    blocks.  GENERIC stage-VM plans are not distributed (UnsupportedPlanError).
     """
     import torch
     import torch.distributed as dist
 
-    from .engine import FeatureMatrix, lower_all, mine_rows_device
+    from . import _lib
+    from .engine import FeatureMatrix, _chunks, lower_all, mine_members_device, mine_rows_device
     from .graph import as_device_graph
 
     plans, descs = lower_all(plans)
     dg = as_device_graph(graph, torch.cuda.current_device())
     side = torch.cuda.Stream()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    E = dg.edge_count
 
-    def block(lo, hi, out):
+    def on_side(fn, out):
         # launch on a non-NULL stream (NULL selects the graph's own stream),
-        # then order the all-gather on the current stream after it
+        # then order the collective on the current stream after it
         side.wait_stream(torch.cuda.current_stream())
         out.record_stream(side)
-        mine_rows_device(dg, descs, lo, hi, out.data_ptr(), side.cuda_stream)
+        fn(out.data_ptr(), side.cuda_stream)
         torch.cuda.current_stream().wait_stream(side)
 
-    full = mine_pipelined(dg.edge_count, len(descs), dist.get_rank(group), dist.get_world_size(group),
-                          block, device="cuda", group=group)
-    values = full.cpu().numpy()
-    return FeatureMatrix(tuple(p.name for p in plans), values, graph.edge_src, graph.edge_dst,
-                         graph.edge_time, getattr(graph, "edge_label", dg.edge_label))
+    values = torch.empty((E, len(descs)), dtype=torch.int64, device="cuda")
+    trig = [i for i, d in enumerate(descs) if not d.members]
+    memb = [i for i, d in enumerate(descs) if d.members]
+    for part in _chunks(trig, _lib.MAX_PLANS):
+        dp = [descs[i] for i in part]
+        full = mine_pipelined(E, len(part), rank, world,
+                              lambda lo, hi, out, dp=dp: on_side(
+                                  lambda ptr, st: mine_rows_device(dg, dp, lo, hi, ptr, st), out),
+                              pieces=pieces, device="cuda", group=group, narrow=narrow)
+        values[:, part] = full
+    for part in _chunks(memb, _lib.MAX_PLANS):
+        dp = [descs[i] for i in part]
+        acc = sum_members(E, len(part), rank, world,
+                          lambda lo, hi, out, dp=dp: on_side(
+                              lambda ptr, st: mine_members_device(dg, dp, lo, hi, ptr, st), out),
+                          device="cuda", group=group)
+        values[:, part] = acc
+    host = values.cpu().numpy()
+    return FeatureMatrix(tuple(p.name for p in plans), host, graph.edge_src, graph.edge_dst,
+                         graph.edge_time, getattr(graph, "edge_label", dg.edge_label), device_graph=dg)

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostmem
 from .graph import DeviceGraph, as_device_graph
 from .plan import BUILTIN_COLUMNS, GENERIC, PlanDesc, lower_plan
 from .vm import VmProgram, lower_program, vm_instance_stream, vm_members, vm_mine
@@ -93,10 +93,11 @@ class FeatureMatrix:
         lab = np.ascontiguousarray(self.edge_label, dtype=np.int8)
         n = ctypes.c_int64()
         lib = _lib.load()
-        _lib.check(lib.tm_csv_format(dg.handle, _lib.ptr(vals), 0, vals.shape[1], _lib.ptr(lab),
-                                     ctypes.byref(n)), "tm_csv_format")
-        buf = np.empty(n.value, dtype=np.uint8)
-        _lib.check(lib.tm_csv_fetch(dg.handle, _lib.ptr(buf), n.value), "tm_csv_fetch")
+        with dg.lock:  # format + fetch share the graph's text buffer: one unit
+            _lib.check(lib.tm_csv_format(dg.handle, _lib.ptr(vals), 0, vals.shape[1], _lib.ptr(lab),
+                                         ctypes.byref(n)), "tm_csv_format")
+            buf = np.empty(n.value, dtype=np.uint8)
+            _lib.check(lib.tm_csv_fetch(dg.handle, _lib.ptr(buf), n.value), "tm_csv_fetch")
         with open(path, "wb") as fh:
             fh.write(("edge_id,src,dst,timestamp,label" + "".join("," + c for c in self.columns)
                       + "\n").encode("utf-8"))
@@ -182,8 +183,9 @@ def mine_members(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int = 0, hi: in
         out[:] = 0
         return out
     arr = _lib.plan_array(descs)
-    rc = _lib.load().tm_mine_members(dgraph.handle, arr, len(descs), lo, hi, _lib.ptr(out), 0, None)
-    _lib.check(rc, "tm_mine_members")
+    with dgraph.lock:
+        rc = _lib.load().tm_mine_members(dgraph.handle, arr, len(descs), lo, hi, _lib.ptr(out), 0, None)
+        _lib.check(rc, "tm_mine_members")
     return out
 
 
@@ -198,8 +200,9 @@ def mine_rows(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int,
     if rows == 0 or not descs:
         return out
     arr = _lib.plan_array(descs)
-    rc = _lib.load().tm_mine(dgraph.handle, arr, len(descs), lo, hi, _lib.ptr(out), 0, None)
-    _lib.check(rc, "tm_mine")
+    with dgraph.lock:
+        rc = _lib.load().tm_mine(dgraph.handle, arr, len(descs), lo, hi, _lib.ptr(out), 0, None)
+        _lib.check(rc, "tm_mine")
     return out
 
 
@@ -207,12 +210,29 @@ def mine_rows_device(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: in
                      stream: int | None = None) -> None:
     """Enqueue rows [lo, hi) into a device int64 buffer at out_ptr (row-major,
     len(descs) columns) on `stream`; returns without synchronizing."""
+    if any(d.members for d in descs):
+        raise ValueError("mine_rows_device takes trigger-attribution columns; use mine_members_device")
     if hi <= lo or not descs:
         return
     arr = _lib.plan_array(descs)
-    rc = _lib.load().tm_mine(dgraph.handle, arr, len(descs), lo, hi, ctypes.c_void_p(out_ptr), 1,
-                             ctypes.c_void_p(stream) if stream else None)
-    _lib.check(rc, "tm_mine")
+    with dgraph.lock:
+        rc = _lib.load().tm_mine(dgraph.handle, arr, len(descs), lo, hi, ctypes.c_void_p(out_ptr), 1,
+                                 ctypes.c_void_p(stream) if stream else None)
+        _lib.check(rc, "tm_mine")
+
+
+def mine_members_device(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int, out_ptr: int,
+                        stream: int | None = None) -> None:
+    """Enqueue members attribution of triggers [lo, hi): contributions are
+    ADDED into the full (n_edges, len(descs)) device block at out_ptr — a
+    sum over trigger ranges, so ranks combine with an all-reduce."""
+    if hi <= lo or not descs:
+        return
+    arr = _lib.plan_array(descs)
+    with dgraph.lock:
+        rc = _lib.load().tm_mine_members(dgraph.handle, arr, len(descs), lo, hi, ctypes.c_void_p(out_ptr), 1,
+                                         ctypes.c_void_p(stream) if stream else None)
+        _lib.check(rc, "tm_mine_members")
 
 
 # triggers per tm_collect_instances call: bounds the device record stream
@@ -227,10 +247,11 @@ def instance_stream(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int
     lib = _lib.load()
     arr = _lib.plan_array(descs)
     words = ctypes.c_int64()
-    _lib.check(lib.tm_collect_instances(dgraph.handle, arr, len(descs), lo, hi, ctypes.byref(words)),
-               "tm_collect_instances")
-    buf = np.empty(words.value, dtype=np.int32)
-    _lib.check(lib.tm_fetch_instances(dgraph.handle, _lib.ptr(buf), words.value), "tm_fetch_instances")
+    with dgraph.lock:  # collect + fetch share the graph's record buffer: one unit
+        _lib.check(lib.tm_collect_instances(dgraph.handle, arr, len(descs), lo, hi, ctypes.byref(words)),
+                   "tm_collect_instances")
+        buf = np.empty(words.value, dtype=np.int32)
+        _lib.check(lib.tm_fetch_instances(dgraph.handle, _lib.ptr(buf), words.value), "tm_fetch_instances")
     return buf
 
 
@@ -267,7 +288,8 @@ def collect_instance_records(dgraph: DeviceGraph, descs: list[PlanDesc], names: 
 
 def last_stats(dgraph: DeviceGraph) -> _lib.TmMineStats:
     st = _lib.TmMineStats()
-    _lib.check(_lib.load().tm_last_mine_stats(dgraph.handle, ctypes.byref(st)), "tm_last_mine_stats")
+    with dgraph.lock:
+        _lib.check(_lib.load().tm_last_mine_stats(dgraph.handle, ctypes.byref(st)), "tm_last_mine_stats")
     return st
 
 
@@ -284,9 +306,14 @@ def mine(graph, plans, workers: int = 1, collect_instances: bool = False, *, dev
     plans, items = lower_all(plans, vocab, allow_vm=True)
     dg = as_device_graph(graph, device)
     E = dg.edge_count
-    values = np.zeros((E, len(items)), dtype=np.int64)
+    # page-locked values: tm_mine overlaps its D2H with mining (hostmem.py)
+    values = hostmem.pinned_empty((E, len(items)), np.int64)
     trig = [i for i, d in enumerate(items) if isinstance(d, PlanDesc) and not d.members]
     memb = [i for i, d in enumerate(items) if isinstance(d, PlanDesc) and d.members]
+    if len(trig) == len(items) and len(items) <= _lib.MAX_PLANS:
+        # the common case: every column in one launch, written in place
+        mine_rows(dg, items, 0, E, out=values)
+        trig = []
     for part in _chunks(trig):
         values[:, part] = mine_rows(dg, [items[i] for i in part], 0, E)
     for part in _chunks(memb):

@@ -9,6 +9,7 @@ are built there by radix sorts (csrc/tm_graph.cu).
 from __future__ import annotations
 
 import ctypes
+import threading
 import weakref
 from dataclasses import dataclass
 
@@ -67,6 +68,9 @@ class DeviceGraph:
         _lib.check(rc, "tm_graph_build")
         self._h = handle
         self._finalizer = weakref.finalize(self, lib.tm_graph_free, handle)
+        # every C call sequence on the handle runs under this lock: the calls
+        # share the handle's scratch and result buffers (tempmine_b200.h)
+        self.lock = threading.RLock()
         self._stats: GraphStats | None = None
         self._csr: dict = {}
         # edge attributes (txgraph.py:113-123), uploaded on first use by an
@@ -90,8 +94,9 @@ class DeviceGraph:
         order = sorted(range(len(vocab)), key=lambda i: vocab[i])
         rank = np.empty(len(vocab), dtype=np.int32)
         rank[order] = np.arange(len(vocab), dtype=np.int32)
-        _lib.check(_lib.load().tm_graph_set_attrs(self.handle, _lib.ptr(amount), _lib.ptr(cur), len(vocab),
-                                                  _lib.ptr(rank)), "tm_graph_set_attrs")
+        with self.lock:
+            _lib.check(_lib.load().tm_graph_set_attrs(self.handle, _lib.ptr(amount), _lib.ptr(cur),
+                                                      len(vocab), _lib.ptr(rank)), "tm_graph_set_attrs")
         self._attrs_on_device = True
 
     @classmethod
@@ -107,6 +112,7 @@ class DeviceGraph:
         self.edge_label = edge_label
         self._h = handle
         self._finalizer = weakref.finalize(self, _lib.load().tm_graph_free, handle)
+        self.lock = threading.RLock()
         self._stats = None
         self._csr = {}
         self.edge_amount = edge_amount
@@ -130,19 +136,22 @@ class DeviceGraph:
         return self._h
 
     def free(self) -> None:
-        if self._h is not None:
-            self._finalizer()
-            self._h = None
+        with self.lock:
+            if self._h is not None:
+                self._finalizer()
+                self._h = None
 
     def info(self) -> _lib.TmGraphInfo:
         info = _lib.TmGraphInfo()
-        _lib.check(_lib.load().tm_graph_info_get(self.handle, ctypes.byref(info)), "tm_graph_info_get")
+        with self.lock:
+            _lib.check(_lib.load().tm_graph_info_get(self.handle, ctypes.byref(info)), "tm_graph_info_get")
         return info
 
     def degrees(self, direction: str) -> np.ndarray:
         out = np.empty(self.node_count, dtype=np.int64)
         d = 1 if direction == "out" else 0
-        _lib.check(_lib.load().tm_graph_degrees(self.handle, d, _lib.ptr(out)), "tm_graph_degrees")
+        with self.lock:
+            _lib.check(_lib.load().tm_graph_degrees(self.handle, d, _lib.ptr(out)), "tm_graph_degrees")
         return out
 
     @property
@@ -167,9 +176,10 @@ class DeviceGraph:
             nbr = np.empty(e, dtype=np.int64)
             tim = np.empty(e, dtype=np.int64)
             eid = np.empty(e, dtype=np.int64)
-            _lib.check(_lib.load().tm_graph_export_csr(self.handle, d, _lib.ptr(indptr), _lib.ptr(nbr),
-                                                       _lib.ptr(tim), _lib.ptr(eid)),
-                       "tm_graph_export_csr")
+            with self.lock:
+                _lib.check(_lib.load().tm_graph_export_csr(self.handle, d, _lib.ptr(indptr), _lib.ptr(nbr),
+                                                           _lib.ptr(tim), _lib.ptr(eid)),
+                           "tm_graph_export_csr")
             for a in (indptr, nbr, tim, eid):
                 a.flags.writeable = False
             self._csr[direction] = (indptr, nbr, tim, eid)

@@ -269,8 +269,10 @@ def vm_mine(dgraph, vp: VmProgram, lo: int = 0, hi: int | None = None):
     out = np.zeros(hi - lo, dtype=np.int64)
     if hi <= lo:
         return out
-    _prepare(dgraph, vp)
-    _lib.check(_lib.load().tm_vm_mine(dgraph.handle, ctypes.byref(vp.prog), lo, hi, _lib.ptr(out)), "tm_vm_mine")
+    with dgraph.lock:
+        _prepare(dgraph, vp)
+        _lib.check(_lib.load().tm_vm_mine(dgraph.handle, ctypes.byref(vp.prog), lo, hi, _lib.ptr(out)),
+                   "tm_vm_mine")
     return out
 
 
@@ -281,9 +283,10 @@ def vm_members(dgraph, vp: VmProgram, lo: int = 0, hi: int | None = None):
     out = np.zeros(dgraph.edge_count, dtype=np.int64)
     if dgraph.edge_count == 0:
         return out
-    _prepare(dgraph, vp)
-    _lib.check(_lib.load().tm_vm_members(dgraph.handle, ctypes.byref(vp.prog), lo, hi, _lib.ptr(out)),
-               "tm_vm_members")
+    with dgraph.lock:
+        _prepare(dgraph, vp)
+        _lib.check(_lib.load().tm_vm_members(dgraph.handle, ctypes.byref(vp.prog), lo, hi, _lib.ptr(out)),
+                   "tm_vm_members")
     return out
 
 
@@ -292,11 +295,12 @@ def vm_instance_stream(dgraph, vp: VmProgram, plan_index: int, lo: int, hi: int)
     import numpy as np
     if hi <= lo:
         return np.zeros(0, dtype=np.int32)
-    _prepare(dgraph, vp)
     lib = _lib.load()
     words = ctypes.c_int64()
-    _lib.check(lib.tm_vm_collect(dgraph.handle, ctypes.byref(vp.prog), plan_index, lo, hi, ctypes.byref(words)),
-               "tm_vm_collect")
-    buf = np.empty(words.value, dtype=np.int32)
-    _lib.check(lib.tm_fetch_instances(dgraph.handle, _lib.ptr(buf), words.value), "tm_fetch_instances")
+    with dgraph.lock:  # collect + fetch share the graph's record buffer: one unit
+        _prepare(dgraph, vp)
+        _lib.check(lib.tm_vm_collect(dgraph.handle, ctypes.byref(vp.prog), plan_index, lo, hi,
+                                     ctypes.byref(words)), "tm_vm_collect")
+        buf = np.empty(words.value, dtype=np.int32)
+        _lib.check(lib.tm_fetch_instances(dgraph.handle, _lib.ptr(buf), words.value), "tm_fetch_instances")
     return buf

@@ -14,7 +14,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2604_12241_b200.distributed import mine_pipelined, mine_sharded, partition, piece_bounds
+from paper_2604_12241_b200.distributed import (mine_pipelined, mine_sharded, partition, piece_bounds,
+                                                sum_members)
 
 
 def test_partition_equal_chunks():
@@ -46,6 +47,15 @@ def _free_port() -> int:
 
 
 def _worker(rank, world, port, src, dst, t, names, delta, q):
+    try:
+        _work(rank, world, port, src, dst, t, names, delta, q)
+    except BaseException as exc:  # report instead of leaving the peer waiting
+        import traceback
+        q.put((rank, traceback.format_exc()))
+        raise
+
+
+def _work(rank, world, port, src, dst, t, names, delta, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.oracle import OracleGraph, column
@@ -58,6 +68,38 @@ def _worker(rank, world, port, src, dst, t, names, delta, q):
     full = mine_sharded(len(src), len(cols), rank, world, block, device="cpu")
     piped = mine_pipelined(len(src), len(cols), rank, world, block, pieces=3, device="cpu")
     assert torch.equal(full, piped)
+    # int32 transport: exact, no piece needs the int64 re-gather
+    st = {}
+    narrow = mine_pipelined(len(src), len(cols), rank, world, block, pieces=3, device="cpu", narrow=True,
+                            stats=st)
+    assert torch.equal(full, narrow) and st["pieces_int64"] == 0
+
+    # a block with counts beyond int32 in one rank's part of piece 1 only:
+    # that piece is re-gathered at full width, the others stay narrow
+    target = piece_bounds(len(src), world, 3)[2][1][1]  # rank 1's part of piece 1
+
+    def big_block(lo, hi, out):
+        block(lo, hi, out)
+        if rank == 1 and (lo, hi) == target:
+            out[: hi - lo, 0] += 3 * 2**31
+
+    want_big = mine_pipelined(len(src), len(cols), rank, world, big_block, pieces=3, device="cpu")
+    st = {}
+    got_big = mine_pipelined(len(src), len(cols), rank, world, big_block, pieces=3, device="cpu", narrow=True,
+                             stats=st)
+    assert torch.equal(want_big, got_big)
+    assert st["pieces_int64"] == 1
+
+    # members-style accumulation: each rank adds its triggers' contributions
+    # into every row; the all-reduce sum equals one process doing all ranges
+    def add_range(lo, hi, acc):
+        for e in range(lo, hi):
+            acc[e, 0] += 1
+            acc[(e * 7) % len(src), 1] += e
+    acc = sum_members(len(src), 2, rank, world, add_range, device="cpu")
+    ref = torch.zeros_like(acc)
+    add_range(0, len(src), ref)
+    assert torch.equal(acc, ref)
     q.put((rank, full.numpy().copy()))
     dist.barrier()
     dist.destroy_process_group()
@@ -81,7 +123,11 @@ def test_two_rank_gather_matches_single(n_edges):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, src, dst, t, names, 60, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=120) for _ in range(2))
+    got = {}
+    for _ in range(2):
+        r, val = q.get(timeout=120)
+        assert not isinstance(val, str), val
+        got[r] = val
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

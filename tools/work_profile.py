@@ -15,10 +15,7 @@ os.environ["TM_LIB"] = os.path.abspath(sys.argv[1])
 import paper_2604_12241_b200 as tmb  # noqa: E402
 from paper_2604_12241_b200 import _lib, synth  # noqa: E402
 
-NAMES = ["trig", "u_walk", "u_item", "v_walk", "v_item", "window", "bisect32", "scan_call",
-         "scan_load", "pair_call", "bisect64", "inner_call", "inner_walk", "chain1", "chain2",
-         "chain3", "chain4", "close_call", "close_walk", "dom_task", "chain_task", "first",
-         "inner_skip", "pulls"]
+NAMES = _lib.COUNTER_NAMES
 
 name = sys.argv[2] if len(sys.argv) > 2 else "hi-small"
 cols = sys.argv[3:] or ["ALL14"]
