@@ -57,10 +57,11 @@ __device__ __forceinline__ int lb_u64(const uint64_t *__restrict__ k, int a, int
 }
 
 struct Ctx {
-  const DevGraph &g;  // a __grid_constant__ kernel parameter
+  const DevGraph &g;  // a __grid_constant__ kernel parameter (global or slab view)
   int u, v;
   uint32_t lo, hi;    // window in rank space
   Win wui, wuo, wvi, wvo;  // trigger windows (u-in, u-out, v-in, v-out)
+  int64_t soff = 0;   // slab view: row of the trigger's slab in the offset table
 };
 
 // Both variants measured slower on HI-Small (4.73 -> 5.25 ms/step,
@@ -94,7 +95,8 @@ __device__ __forceinline__ int ub_gallop(const uint32_t *__restrict__ r, int s, 
 // windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
 __device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
   TM_CNT(kCtrWin, 1);
-  const int a = __ldg(c.g.ptr[dir] + x), b = __ldg(c.g.ptr[dir] + x + 1);
+  const int32_t *pt = c.g.ptr[dir] + c.soff;
+  const int a = __ldg(pt + x), b = __ldg(pt + x + 1);
 #if TM_WIN_PAR
   // both bounds bisected at once: two independent load chains in flight
   const uint32_t *__restrict__ r = c.g.rnk[dir];
@@ -137,8 +139,8 @@ __device__ __forceinline__ void fill_windows(Ctx &c, int need) {
     const int dir = i & 1, x = (i >> 1) ? c.v : c.u;
     r[i] = c.g.rnk[dir];
     const bool on = (need >> i) & 1;
-    a[i] = on ? __ldg(c.g.ptr[dir] + x) : 0;
-    b[i] = on ? __ldg(c.g.ptr[dir] + x + 1) : 0;
+    a[i] = on ? __ldg(c.g.ptr[dir] + c.soff + x) : 0;
+    b[i] = on ? __ldg(c.g.ptr[dir] + c.soff + x + 1) : 0;
     e[i] = b[i];
   }
   while (a[0] < b[0] || a[1] < b[1] || a[2] < b[2] || a[3] < b[3]) {
@@ -162,7 +164,7 @@ __device__ __forceinline__ void fill_windows(Ctx &c, int need) {
 __device__ __forceinline__ int loops_in_window(const Ctx &c, int x, int has_loop = -1) {
   if (has_loop < 0) has_loop = __ldg(c.g.loop + x);
   if (!has_loop) return 0;
-  const int a = __ldg(c.g.ptr[1] + x), b = __ldg(c.g.ptr[1] + x + 1);
+  const int a = __ldg(c.g.gptr[1] + x), b = __ldg(c.g.gptr[1] + x + 1);
   const uint64_t base = (uint64_t)(uint32_t)x << c.g.rank_bits;
   return lb_u64(c.g.pkey[1], a, b, base + c.hi + 1) - lb_u64(c.g.pkey[1], a, b, base + c.lo);
 }
@@ -172,7 +174,7 @@ __device__ __forceinline__ int loops_in_window(const Ctx &c, int x, int has_loop
 // lies before lo (prev = rank + 1, 0 = none)
 __device__ __forceinline__ bool first_in_window(const Ctx &c, int dir, int j) {
   TM_CNT(kCtrFirst, 1);
-  return __ldg(c.g.prev[dir] + j) <= c.lo;
+  return (uint32_t)__ldg(c.g.np[dir] + j).y <= c.lo;
 }
 
 // (neighbour, prev) of CSR slot j in one 8-byte load: the walkers read both
@@ -197,7 +199,7 @@ constexpr int kScanWin = TM_SCAN_WIN;
 // (n in N^dir(x)  <=>  x in N^{1-dir}(n)).  Needs no window of x.
 __device__ __forceinline__ bool exists_pair(const Ctx &c, int dir, int x, int xs, int xe, int n) {
   TM_CNT(kCtrPairCall, 1);
-  const int ns = __ldg(c.g.ptr[dir ^ 1] + n), ne = __ldg(c.g.ptr[dir ^ 1] + n + 1);
+  const int ns = __ldg(c.g.gptr[dir ^ 1] + n), ne = __ldg(c.g.gptr[dir ^ 1] + n + 1);
   const bool from_x = xe - xs <= ne - ns;
   const uint64_t *k = c.g.pkey[from_x ? dir : dir ^ 1];
   const int s = from_x ? xs : ns, e = from_x ? xe : ne;
@@ -206,32 +208,47 @@ __device__ __forceinline__ bool exists_pair(const Ctx &c, int dir, int x, int xs
   return q < e && __ldg(k + q) <= base + c.hi;
 }
 
-// does x's dir-window w contain neighbour n?  Windows are time-local and
-// short: scan them.  A wide w (a hub) is answered from the pair index.
-__device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
-  if (w.len() <= kScanWin) {
-    TM_CNT(kCtrScanCall, 1);
-    bool hit = false;
+// is n among the entries of window w of direction dir?  (short windows)
+__device__ __forceinline__ bool scan_for(const Ctx &c, int dir, const Win &w, int n) {
+  TM_CNT(kCtrScanCall, 1);
+  bool hit = false;
 #if TM_SCAN4
-    // four independent loads per round trip (the early exit only every 4)
-    const int32_t *__restrict__ nb = c.g.nbr[dir];
-    for (int j = w.a; j < w.b && !hit; j += 4) {
-      TM_CNT(kCtrScanLoad, 1);
-      const int x0 = __ldg(nb + j);
-      const int x1 = j + 1 < w.b ? __ldg(nb + j + 1) : -1;
-      const int x2 = j + 2 < w.b ? __ldg(nb + j + 2) : -1;
-      const int x3 = j + 3 < w.b ? __ldg(nb + j + 3) : -1;
-      hit = (x0 == n) | (x1 == n) | (x2 == n) | (x3 == n);
-    }
-#else
-    for (int j = w.a; j < w.b && !hit; ++j) {
-      TM_CNT(kCtrScanLoad, 1);
-      hit = __ldg(c.g.nbr[dir] + j) == n;
-    }
-#endif
-    return hit;
+  // four independent loads per round trip (the early exit only every 4)
+  const int2 *__restrict__ nb = c.g.np[dir];
+  for (int j = w.a; j < w.b && !hit; j += 4) {
+    TM_CNT(kCtrScanLoad, 1);
+    const int x0 = __ldg(nb + j).x;
+    const int x1 = j + 1 < w.b ? __ldg(nb + j + 1).x : -1;
+    const int x2 = j + 2 < w.b ? __ldg(nb + j + 2).x : -1;
+    const int x3 = j + 3 < w.b ? __ldg(nb + j + 3).x : -1;
+    hit = (x0 == n) | (x1 == n) | (x2 == n) | (x3 == n);
   }
-  return exists_pair(c, dir, x, __ldg(c.g.ptr[dir] + x), __ldg(c.g.ptr[dir] + x + 1), n);
+#else
+  for (int j = w.a; j < w.b && !hit; ++j) {
+    TM_CNT(kCtrScanLoad, 1);
+    hit = __ldg(c.g.np[dir] + j).x == n;
+  }
+#endif
+  return hit;
+}
+
+#ifndef TM_SLAB_PROBE
+#define TM_SLAB_PROBE 1
+#endif
+
+// does x's dir-window w contain neighbour n?  Windows are time-local and
+// short: scan them.  A wide w (a hub): in a slab view n's opposite window
+// (x in N^{1-dir}(n)) is a short slab run — scan that; else (or when that is
+// wide too) one bisection of the shorter pair-index run.
+__device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
+  if (w.len() <= kScanWin) return scan_for(c, dir, w, n);
+#if TM_SLAB_PROBE
+  if (c.g.ptr[dir ^ 1] != c.g.gptr[dir ^ 1]) {
+    const Win wn = window(c, dir ^ 1, n);
+    if (wn.len() <= kScanWin) return scan_for(c, dir ^ 1, wn, x);
+  }
+#endif
+  return exists_pair(c, dir, x, __ldg(c.g.gptr[dir] + x), __ldg(c.g.gptr[dir] + x + 1), n);
 }
 
 __device__ __forceinline__ long long warp_sum(long long x) {

@@ -83,6 +83,16 @@ __global__ void k_rank_scatter(const uint64_t *__restrict__ k, const uint32_t *_
   rank[ids[i]] = r;
 }
 
+// ids sorted by time -> the time-order array; flags any id out of place
+__global__ void k_time_order(const uint32_t *__restrict__ ids, int64_t n, int32_t *__restrict__ order,
+                             unsigned int *__restrict__ moved) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t e = ids[i];
+  order[i] = (int32_t)e;
+  if (e != (uint32_t)i) *moved = 1u;  // benign race: every writer stores 1
+}
+
 __global__ void k_csr_keys(const int32_t *__restrict__ owner, const uint32_t *__restrict__ rank,
                            int64_t n, int rbits, uint64_t *__restrict__ keys,
                            uint32_t *__restrict__ ids) {
@@ -236,6 +246,7 @@ tmb::DevGraph tm_graph::dev() const {
     g.peid[d] = peid[d].as<int32_t>();
     g.np[d] = npk[d].as<int2>();
     g.owner[d] = owner[d].as<int32_t>();
+    g.gptr[d] = g.ptr[d];
   }
   g.loop = loop.as<uint8_t>();
   return g;
@@ -297,6 +308,7 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
   TM_CUDA(cudaStreamSynchronize(s));
   if (h1.bad) return fail(TM_E_BAD_ARG, std::to_string(h1.bad) + " edge endpoint(s) outside [0, n_nodes)");
   g->n_selfloops = (int64_t)h1.selfloops;
+  g->t_min = (int64_t)h1.tmin;
   g->t_span = (int64_t)((unsigned long long)h1.tmax - (unsigned long long)h1.tmin);
 
   // 2. narrow ids, time keys
@@ -339,6 +351,17 @@ static int build_impl(tm_graph *g, const int64_t *src, const int64_t *dst, const
   k_rank_scatter<<<grid_for(E, kB), kB, 0, s>>>(ks, vs, flags, E, h1.tmin,
                                                 g->uniq_time.as<int64_t>(), g->e_rank.as<uint32_t>());
   TM_LAUNCHED("k_rank_scatter");
+  {  // edge ids in time order (the stable sort keeps id order within a timestamp)
+    if ((rc = g->time_order.ensure_on(4 * E, s))) return rc;
+    unsigned int moved = 0;
+    unsigned int *d_moved = reinterpret_cast<unsigned int *>(st.p);  // ScanStats is no longer needed
+    TM_CUDA(cudaMemsetAsync(d_moved, 0, sizeof(unsigned int), s));
+    k_time_order<<<grid_for(E, kB), kB, 0, s>>>(vs, E, g->time_order.as<int32_t>(), d_moved);
+    TM_LAUNCHED("k_time_order");
+    TM_CUDA(cudaMemcpyAsync(&moved, d_moved, sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaStreamSynchronize(s));
+    g->ids_time_ordered = moved == 0;
+  }
   g->rank_bits = std::max(1, bits_for((uint64_t)(g->n_ranks - 1)));
   g->node_bits = std::max(1, bits_for((uint64_t)(N - 1)));
   if (g->rank_bits + g->node_bits > 63 || 2 * g->node_bits > 64)
@@ -432,7 +455,7 @@ extern "C" int tm_graph_build(int device, int64_t n_nodes, int64_t n_edges, cons
     return rc;
   }
   int64_t bytes = 0;
-  for (const DevBuf *b : {&g->e_src, &g->e_dst, &g->e_rank, &g->uniq_time, &g->loop})
+  for (const DevBuf *b : {&g->e_src, &g->e_dst, &g->e_rank, &g->uniq_time, &g->loop, &g->time_order})
     bytes += (int64_t)b->bytes;
   for (int d = 0; d < 2; ++d)
     for (const DevBuf *b : {&g->ptr[d], &g->nbr[d], &g->rnk[d], &g->eid[d], &g->pkey[d], &g->prev[d], &g->peid[d],

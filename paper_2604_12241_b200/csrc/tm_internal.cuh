@@ -22,6 +22,17 @@
 //                    the window [lo, hi] (np.unique dedup, kernels.py:59)
 //                    iff prev[j] <= lo: one coalesced load along the window.
 //   self-loop flags  loop uint8[N] (txgraph.py:146-153 self-loop CSR)
+//
+// Time-slab view (tm_slab.cu, built per mining call and delta): the time
+// axis is cut into slabs of width W >= delta; slab s holds, per node, the
+// sub-run of edges with rank in [L_s, S_{s+1}) — its own triggers' ranks
+// [S_s, S_{s+1}) plus a halo back to the earliest window start L_s.  Every
+// window of a trigger in slab s lies inside that slab's run, so the mining
+// kernels read short, time-local runs from a few-% slice of the edge arrays
+// (L2-resident) instead of bisecting whole-horizon runs.  A DevGraph whose
+// ptr / np / rnk point at a slab index is a "slab view": ptr is then the
+// [n_slabs][N+1] offset table (Ctx::soff selects the slab) and gptr keeps
+// the global offsets for the pair index (pkey runs).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -54,6 +65,7 @@ struct DevGraph {
   const int2 *np[2];       // (nbr, prev) per CSR slot, interleaved for the walkers
   const int32_t *owner[2]; // owner node of each CSR slot (slot-parallel window sweeps)
   const uint8_t *loop;
+  const int32_t *gptr[2];  // global CSR offsets: pair-index runs (== ptr in the global view)
 };
 
 constexpr int kMaxChain = 5;   // cycle_8: chain a1..a5
@@ -81,6 +93,12 @@ struct CycGroup {
 // the columns sharing one delta: one set of trigger windows, one
 // lower-bound table, one pass over each trigger slice
 struct DevGroup {
+  // the graph as this group's kernels read it: the global CSR, or the time-
+  // slab view of the group's delta (tm_slab.cu); slab_of[rank] selects the
+  // slab (null: global view), its offset table row is slab * stride
+  DevGraph view;
+  const uint16_t *slab_of;
+  int64_t stride;
   const uint32_t *lo_tab;  // rank -> first rank with time >= uniq_time[rank] - delta
   // own windows by edge id (or null): own[1][e] = window of e's source
   // out-run at e's time (u-out), own[0][e] = of e's destination in-run (v-in)
@@ -172,6 +190,23 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *v
 // exclusive scan of uint32 counts (n <= 2^31) into out (may alias in)
 int exclusive_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, cudaStream_t s);
 
+// ----------------------------------------------------------------- slabs
+
+constexpr int kMaxSlabs = 128;  // slab offset tables are [n_slabs][N+1]
+constexpr int kMinSlabs = 3;    // fewer slabs than this: the global view is used
+
+// one delta's slab index (grow-only device storage, tm_slab.cu)
+struct SlabIndex {
+  DevBuf start[2];   // [n_slabs][N+1] global CSR slot of each slab run's first entry
+  DevBuf ptr[2];     // [n_slabs][N+1] slab run offsets (exclusive scan of the run lengths)
+  DevBuf np[2];      // (nbr, prev) per slab entry
+  DevBuf rnk[2];     // rank per slab entry
+  DevBuf slab_of;    // uint16 [R]: slab of each rank
+  DevBuf bounds;     // uint32 [2][n_slabs + 1]: S_s (first trigger rank), L_s (first halo rank)
+  int n_slabs = 0;
+  int64_t entries[2] = {0, 0};
+};
+
 inline int bits_for(uint64_t maxval) {  // bits to represent [0, maxval]
   int b = 0;
   while (b < 64 && (maxval >> b) != 0) ++b;
@@ -218,6 +253,10 @@ struct tm_graph {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t piece_ev[8] = {};
   tmb::DevBuf split_counts;
+  tmb::SlabIndex slabs[tmb::kMaxGroups];
+  int64_t t_min = 0;   // smallest timestamp (ticks)
+  tmb::DevBuf time_order;         // int32[E]: edge ids sorted by (time, id)
+  bool ids_time_ordered = false;  // time_order is the identity
   // completion of the last call that enqueued work on a (possibly user)
   // stream: the next call's stream waits on it before touching the shared
   // scratch, and tm_graph_free waits on it before freeing
@@ -234,3 +273,12 @@ struct tm_graph {
 
   tmb::DevGraph dev() const;
 };
+
+namespace tmb {
+// The slab view of delta group k for this call: builds the slab index of
+// `delta` into g->slabs[k] on stream s and fills *view / *slab_of / *stride
+// (the global view when the horizon holds fewer than kMinSlabs windows).
+// lo_tab is the group's rank -> window-start table.
+int build_slab_view(tm_graph *g, int k, int64_t delta, const uint32_t *lo_tab, cudaStream_t s,
+                    DevGraph *view, const uint16_t **slab_of, int64_t *stride);
+}  // namespace tmb

@@ -93,7 +93,7 @@ struct TaskBloom;
 
 struct Queue {
   Task *q;
-  int32_t *count;
+  unsigned long long *count;  // 64-bit: reservations past a full queue cannot wrap it
   int32_t cap;
   const TaskBloom *bloom;  // null: no filtering (warp kernel, small windows)
 };
@@ -123,17 +123,21 @@ __device__ __forceinline__ bool bloom_has(const uint32_t *w, int x) {
   return (w[b >> 5] >> (b & 31)) & 1u;
 }
 
-// reserve n slots of the queue, or none: the count never passes the
-// capacity (a plain atomicAdd past a full queue could wrap the int32 count
-// on hub windows and turn later reservations into out-of-bounds writes)
+// reserve n slots of the queue, or none (-1).  The count is 64-bit, so the
+// increments of reservations that fail past a full queue cannot wrap it into
+// a small (or negative) index; a failed reservation that straddles the end
+// marks its slots below the capacity empty (the consumer reads min(count,
+// cap) slots).  A plain atomicAdd: a CAS loop serialized the many emitters
+// of a long-window step (HI-Large cycles: 2.7x slower).
 __device__ __forceinline__ int reserve(const Queue &qu, int n) {
-  int cur = *(volatile int32_t *)qu.count;
-  while (true) {
-    if (cur > qu.cap - n) return -1;
-    const int seen = atomicCAS(qu.count, cur, cur + n);
-    if (seen == cur) return cur;
-    cur = seen;
+  const unsigned long long cap = (unsigned long long)qu.cap;
+  if (*(volatile unsigned long long *)qu.count >= cap) return -1;
+  const unsigned long long base = atomicAdd(qu.count, (unsigned long long)n);
+  if (base + (unsigned long long)n > cap) {
+    for (unsigned long long k = base; k < cap; ++k) qu.q[k].row = -1;  // holes stay empty
+    return -1;
   }
+  return (int)base;
 }
 
 // cut [a, b) into kTaskSpan pieces; false (caller walks it itself) when the
@@ -204,8 +208,10 @@ __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, in
     TM_CNT(kCtrInnerSkip, 1);
     return hits;
   }
-  const int xs = __ldg(c.g.ptr[dx] + x), xe = __ldg(c.g.ptr[dx] + x + 1);
-  if (xe - xs > kLazyRun && wy.len() <= kLazyRun) {
+  const int32_t *pt = c.g.ptr[dx] + c.soff;  // x's run (slab view: its slab run)
+  const int xa = __ldg(pt + x), xb = __ldg(pt + x + 1);
+  if (xb - xa > kLazyRun && wy.len() <= kLazyRun) {
+    const int xs = __ldg(c.g.gptr[dx] + x), xe = __ldg(c.g.gptr[dx] + x + 1);  // pair-index run
     for (int j = wy.a; j < wy.b && hits < K; ++j) {
       TM_CNT(kCtrInnerWalk, 1);
       const int2 sl = slot_np(c, dy, j);
@@ -215,8 +221,8 @@ __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, in
     }
     return hits;
   }
-  const int wa = lb_u32(c.g.rnk[dx], xs, xe, c.lo);
-  const Win wx{wa, ub_u32(c.g.rnk[dx], wa, xe, c.hi)};
+  const int wa = lb_u32(c.g.rnk[dx], xa, xb, c.lo);
+  const Win wx{wa, ub_u32(c.g.rnk[dx], wa, xb, c.hi)};
   TM_CNT(kCtrWin, 1);
   const bool walk_x = wx.len() <= wy.len();
   const Win w = walk_x ? wx : wy;
@@ -300,15 +306,15 @@ __device__ __forceinline__ bool bset_add(int *node, int from, int &n, int m) {
 // the useful depth-J nodes (layers 2 + d - J for the closing depths d >= J
 // in mask), or -1 when a set overflows.  Out of line: it runs for wide
 // chain nodes only and keeps its arrays off the walkers' registers.
-__device__ __noinline__ int useful_nodes(const DevGraph &g, int u, int v, uint32_t lo, uint32_t hi,
-                                         int wa, int wb, int mask, int maxd, int J, int *use) {
-  const Ctx c{g, u, v, lo, hi, {wa, wb}, {}, {}, {}};
+__device__ __noinline__ int useful_nodes(const DevGraph &g, int64_t soff, int u, int v, uint32_t lo,
+                                         uint32_t hi, int wa, int wb, int mask, int maxd, int J, int *use) {
+  const Ctx c{g, u, v, lo, hi, {wa, wb}, {}, {}, {}, soff};
   const int H = 2 + maxd - J;  // deepest layer any useful depth-J node can be in
   int node[kBCap], lend[kMaxChain + 3];
   int n = 0;
   lend[0] = 0;
   for (int j = wa; j < wb; ++j) {  // B_1
-    const int m = __ldg(g.nbr[0] + j);
+    const int m = __ldg(g.np[0] + j).x;
     if (m == u || m == v || !first_in_window(c, 0, j)) continue;
     if (!bset_add(node, 0, n, m)) return TM_CNT(kCtrUsefulOver, 1), -1;
   }
@@ -318,7 +324,7 @@ __device__ __noinline__ int useful_nodes(const DevGraph &g, int u, int v, uint32
       const Win w = window(c, 0, node[i]);
       if (w.len() > kBCap) return TM_CNT(kCtrUsefulOver, 1), -1;
       for (int j = w.a; j < w.b; ++j) {
-        const int m = __ldg(g.nbr[0] + j);
+        const int m = __ldg(g.np[0] + j).x;
         if (m == u || m == v || !first_in_window(c, 0, j)) continue;
         if (!bset_add(node, lend[k - 1], n, m)) return TM_CNT(kCtrUsefulOver, 1), -1;
       }
@@ -339,7 +345,7 @@ __device__ __noinline__ int useful_nodes(const DevGraph &g, int u, int v, uint32
 // (ja, jb, cand) set when the backward sets are much smaller than w
 __device__ __forceinline__ bool pull_candidates(const Ctx &c, const CycGroup &cg, int maxd, int J,
                                                 const Win &w, int *use, int &ja, int &jb) {
-  const int nu = useful_nodes(c.g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, maxd, J, use);
+  const int nu = useful_nodes(c.g, c.soff, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, maxd, J, use);
   if (nu < 0 || nu * 4 > w.len()) return false;
   TM_CNT(kCtrPull, 1);
   ja = 0;
@@ -387,8 +393,8 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
   const int owner = path[L - 1];
   int os = 0, oe = 0;
   if (cand) {
-    os = __ldg(c.g.ptr[1] + owner);
-    oe = __ldg(c.g.ptr[1] + owner + 1);
+    os = __ldg(c.g.gptr[1] + owner);  // pair-index run of the owner
+    oe = __ldg(c.g.gptr[1] + owner + 1);
   }
   // layers a depth-(L+1) node must meet: B_{1+d-L} for closing depths d
   int need = 0;
@@ -545,6 +551,7 @@ struct WarpShared {
   int excl[32];
   int sa[32], sc[32];
   int c3[32];  // cycle_3 raw count (low bits) | V-item parts the warp walks << kPartsShift
+  int slab[32];  // slab of the trigger (slab view of the group)
 };
 constexpr int kPartsShift = 28;  // c3 counts stay far below 2^28 (an in-window degree)
 
@@ -561,8 +568,14 @@ struct SmemSink {  // contributions of row `owner` into the warp's shared state
   __device__ __forceinline__ void c3() { atomicAdd(&ws.c3[owner], 1); }
 };
 
-__device__ __forceinline__ Ctx ctx_of(const DevGraph &g, const WarpShared &ws, int o) {
-  return Ctx{g, ws.u[o], ws.v[o], ws.lo[o], ws.hi[o], ws.wui[o], ws.wuo[o], ws.wvi[o], ws.wvo[o]};
+__device__ __forceinline__ Ctx ctx_of(const DevGroup &gr, const WarpShared &ws, int o) {
+  return Ctx{gr.view, ws.u[o], ws.v[o], ws.lo[o], ws.hi[o], ws.wui[o], ws.wuo[o], ws.wvi[o], ws.wvo[o],
+             (int64_t)ws.slab[o] * gr.stride};
+}
+
+// slab of rank r in the group's view (0 in the global view)
+__device__ __forceinline__ int slab_of(const DevGroup &gr, uint32_t r) {
+  return gr.slab_of ? (int)__ldg(gr.slab_of + r) : 0;
 }
 
 // owner lane of flattened item k: the last lane whose exclusive prefix <= k
@@ -633,7 +646,8 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
 
   for (int gi = 0; gi < P.ngroups; ++gi) {
     const DevGroup &gr = P.gr[gi];
-    Ctx c{g, u, v, valid ? __ldg(gr.lo_tab + r) : 1u, r, {}, {}, {}, {}};
+    const int slab = valid ? slab_of(gr, r) : 0;
+    Ctx c{gr.view, u, v, valid ? __ldg(gr.lo_tab + r) : 1u, r, {}, {}, {}, {}, (int64_t)slab * gr.stride};
     if (valid) trigger_windows(c, gr, (int)row);
     // per-lane columns: fan / degree (kernels.py:290-303), cycle_2 (:320-322)
     if (valid) {
@@ -655,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
       }
     }
     if (!gr.udom && !gr.vdom) continue;
-    ws.u[lane] = u; ws.v[lane] = v; ws.lo[lane] = c.lo; ws.hi[lane] = c.hi;
+    ws.u[lane] = u; ws.v[lane] = v; ws.lo[lane] = c.lo; ws.hi[lane] = c.hi; ws.slab[lane] = slab;
     ws.wui[lane] = c.wui; ws.wuo[lane] = c.wuo; ws.wvi[lane] = c.wvi; ws.wvo[lane] = c.wvo;
     ws.sa[lane] = ws.sc[lane] = 0;
     int vparts = kVAll;
@@ -696,12 +710,12 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
     ws.c3[lane] = vparts << kPartsShift;
     __syncwarp();
     flat_for(ws, lane, ulen, [&](int o, int k) {
-      const Ctx co = ctx_of(g, ws, o);
+      const Ctx co = ctx_of(gr, ws, o);
       SmemSink sk{ws, stage, P.slot, o, S};
       u_item(co, P, gr, co.wui.a + k, sk);
     });
     flat_for(ws, lane, vlen, [&](int o, int k) {
-      const Ctx co = ctx_of(g, ws, o);
+      const Ctx co = ctx_of(gr, ws, o);
       SmemSink sk{ws, stage, P.slot, o, S};
       const int j = co.wvo.a + k;
       const int2 sl = slot_np(co, 1, j);
@@ -776,7 +790,7 @@ __device__ __forceinline__ bool pull_gs(const Ctx &c, const DevPlans &P, const D
   if (ok && lane == 0) {
     int pd[kPairs], np = 0;
     for (int j = c.wuo.a; j < c.wuo.b && ok; ++j) {
-      const int n = __ldg(c.g.nbr[1] + j);
+      const int n = __ldg(c.g.np[1] + j).x;
       if (n == c.u || n == c.v || !first_in_window(c, 1, j)) continue;
       const Win w = window(c, 1, n);
       if (np + w.len() > kPairs) {
@@ -784,7 +798,7 @@ __device__ __forceinline__ bool pull_gs(const Ctx &c, const DevPlans &P, const D
         break;
       }
       for (int k = w.a; k < w.b; ++k) {
-        const int d = __ldg(c.g.nbr[1] + k);
+        const int d = __ldg(c.g.np[1] + k).x;
         if (d == c.u || d == c.v || d == n || !first_in_window(c, 1, k)) continue;
         pd[np++] = d;
       }
@@ -875,7 +889,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q,
     int32_t *__restrict__ bloom_lists) {
-  const int n = min((unsigned)*in.count, (unsigned)in.cap);
+  const int n = (int)min(*in.count, (unsigned long long)in.cap);
   const int warps = gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   __shared__ TaskBloom blooms[kTaskThreads / 32];
@@ -888,7 +902,8 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const int e = (int)(lo + t.row);
     const DevGroup &gr = P.gr[t.grp];
     const uint32_t r = __ldg(g.e_rank + e);
-    Ctx c{g, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {}};
+    Ctx c{gr.view, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {},
+          (int64_t)slab_of(gr, r) * gr.stride};
     trigger_windows(c, gr, t.row);
     // chain walks of this task get the trigger's backward-layer filters
     Queue next = next_q;
@@ -908,14 +923,15 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
       GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
       int parts = t.pad0, ja = t.a, jb = t.b;
       const int *cand = nullptr;
-      const int vs = __ldg(g.ptr[1] + c.v), ve = __ldg(g.ptr[1] + c.v + 1);
+      const int vs = __ldg(g.gptr[1] + c.v), ve = __ldg(g.gptr[1] + c.v + 1);  // v's pair-index run
       if (t.level == kLvlPullV) {
         int redo = 0;
         parts = 0;
         if (gr.n_gs > 0 && !pull_gs(c, P, gr, vs, ve, lane, orow)) redo |= kVGs;
         const CycGroup &cg = gr.cyc;
         if (cg.maxd >= 1 && c.u != c.v && c.wui.len() > 0) {
-          const int nu = useful_nodes(g, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, cg.maxd, 1, use);
+          const int nu = useful_nodes(c.g, c.soff, c.u, c.v, c.lo, c.hi, c.wui.a, c.wui.b, cg.mask, cg.maxd, 1,
+                                      use);
           if (nu < 0 || nu * 4 > t.b - t.a) {
             redo |= kVCyc;
           } else {
@@ -934,7 +950,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
           if (!__shfl_sync(0xffffffffu, ok, 0)) {  // queue full: this warp walks the declined parts too
             if (cand) {
               for (int j = t.a + lane; j < t.b; j += 32) {
-                const int m = __ldg(g.nbr[1] + j);
+                const int m = __ldg(c.g.np[1] + j).x;
                 if (m == c.u || m == c.v || !first_in_window(c, 1, j)) continue;
                 if (redo & kVGs) v_node<true>(c, P, gr, t.grp, t.row, m, sk, next, kVGs);
               }
@@ -1047,6 +1063,27 @@ __global__ void k_own_windows(const __grid_constant__ DevGraph g, const uint32_t
   const uint32_t r = __ldg(rk + p);
   const int lb = lb_u32(rk, a, (int)p, __ldg(lo_tab + r));
   tab[e - lo] = make_int2(lb, ub_gallop(rk, (int)p + 1, b, r));
+}
+
+// the same tables in a slab view: slot p's copy in its own slab sits at
+// sptr[s][x] + (p - start[s][x]); the window is searched inside that short
+// slab run (tm_slab.cu)
+__global__ void k_own_windows_slab(const __grid_constant__ DevGraph g, const uint32_t *__restrict__ lo_tab,
+                                   int dir, int64_t lo, int64_t hi, const uint16_t *__restrict__ slab_of,
+                                   int64_t stride, const int32_t *__restrict__ start,
+                                   const int32_t *__restrict__ sptr, const uint32_t *__restrict__ srnk,
+                                   int2 *__restrict__ tab) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= g.n_edges) return;
+  const int e = __ldg(g.eid[dir] + p);
+  if (e < lo || e >= hi) return;
+  const int x = __ldg(g.owner[dir] + p);
+  const uint32_t r = __ldg(g.rnk[dir] + p);
+  const int64_t cell = (int64_t)__ldg(slab_of + r) * stride + x;
+  const int a = __ldg(sptr + cell), b = __ldg(sptr + cell + 1);
+  const int q = a + (int)(p - __ldg(start + cell));
+  const int lb = lb_u32(srnk, a, q, __ldg(lo_tab + r));
+  tab[e - lo] = make_int2(lb, ub_gallop(srnk, q + 1, b, r));
 }
 
 }  // namespace
@@ -1166,11 +1203,30 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     k_lo_table<<<grid_for(R, 256), 256, 0, s>>>(g->uniq_time.as<int64_t>(), R, deltas[k],
                                                 g->lo_tabs.as<uint32_t>() + (size_t)k * R);
     TM_LAUNCHED("k_lo_table");
+    // the group's view of the graph: time slabs when the call covers a good
+    // share of the edges (the view costs O(E + n_slabs N) to build)
+    if (rows * 16 >= E) {
+      if ((rc = build_slab_view(g, k, deltas[k], dp.gr[k].lo_tab, s, &dp.gr[k].view, &dp.gr[k].slab_of,
+                                &dp.gr[k].stride)))
+        return rc;
+    } else {
+      dp.gr[k].view = dg;
+      dp.gr[k].slab_of = nullptr;
+      dp.gr[k].stride = 0;
+    }
     for (int dir = 0; dir < 2 && own_on; ++dir) {
       if (!((dp.gr[k].need >> (dir ? 1 : 2)) & 1)) continue;
       int2 *tab = g->own_tabs.as<int2>() + (size_t)rows * own_i++;
-      k_own_windows<<<grid_for(E, 256), 256, 0, s>>>(dg, dp.gr[k].lo_tab, dir, lo, hi, tab);
-      TM_LAUNCHED("k_own_windows");
+      if (dp.gr[k].slab_of) {
+        const DevGraph &v = dp.gr[k].view;
+        k_own_windows_slab<<<grid_for(E, 256), 256, 0, s>>>(dg, dp.gr[k].lo_tab, dir, lo, hi, dp.gr[k].slab_of,
+                                                            dp.gr[k].stride, g->slabs[k].start[dir].as<int32_t>(),
+                                                            v.ptr[dir], v.rnk[dir], tab);
+        TM_LAUNCHED("k_own_windows_slab");
+      } else {
+        k_own_windows<<<grid_for(E, 256), 256, 0, s>>>(dg, dp.gr[k].lo_tab, dir, lo, hi, tab);
+        TM_LAUNCHED("k_own_windows");
+      }
       dp.gr[k].own[dir] = tab;
     }
     // Hand-off width for chain nodes: with short windows (mean windowed
@@ -1204,15 +1260,17 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
 #else
   const int64_t split_cap = std::min<int64_t>(std::max<int64_t>(1 << 16, rows / 16), 1 << 22);
 #endif
-  if ((rc = g->heavy_n.ensure_pooled(sizeof(int32_t) * 4, s, g->stream)) ||
+  if ((rc = g->heavy_n.ensure_pooled(sizeof(unsigned long long) * 4, s, g->stream)) ||
       (rc = g->heavy_q.ensure_pooled(sizeof(int32_t) * 2 * (size_t)split_cap, s, g->stream)) ||
       (rc = g->split_scratch.ensure_pooled(sizeof(int32_t) * 3 * (size_t)split_cap, s, g->stream)) ||
       (rc = g->tasks.ensure_pooled(sizeof(Task) * (size_t)task_cap * 2, s, g->stream)))
     return rc;
-  int32_t *cnt = g->heavy_n.as<int32_t>();  // [0] split rows, [1] [2] task queues A / B
-  TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
-  Queue qa{g->tasks.as<Task>(), cnt + 1, (int32_t)task_cap, nullptr};
-  Queue qb{g->tasks.as<Task>() + task_cap, cnt + 2, (int32_t)task_cap, nullptr};
+  // [0] split rows (int32 in the low word), [1] [2] task queues A / B
+  unsigned long long *cnt64 = g->heavy_n.as<unsigned long long>();
+  int32_t *cnt = reinterpret_cast<int32_t *>(cnt64);
+  TM_CUDA(cudaMemsetAsync(cnt64, 0, sizeof(unsigned long long) * 4, s));
+  Queue qa{g->tasks.as<Task>(), cnt64 + 1, (int32_t)task_cap, nullptr};
+  Queue qb{g->tasks.as<Task>() + task_cap, cnt64 + 2, (int32_t)task_cap, nullptr};
 
   for (int i = 0; i < n_plans; ++i) {
     const int f = plans[i].family;
@@ -1257,17 +1315,25 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
     for (int k = 0; k < dpp.ngroups; ++k)
       for (int d = 0; d < 2; ++d)
         if (dpp.gr[k].own[d]) dpp.gr[k].own[d] += r0;
-    TM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
+    TM_CUDA(cudaMemsetAsync(cnt64, 0, sizeof(unsigned long long) * 4, s));
     // full-range device-output calls process triggers in out-CSR order
-    const int32_t *order = (pieces == 1 && lo == 0 && hi == g->n_edges && source_order())
-                               ? g->eid[1].as<int32_t>() : nullptr;
+    // full-range device-output calls: triggers in time order when the edge
+    // ids are not (slab views are then read slab by slab), or out-CSR order
+    // (TM_ORDER=1 A/B); rows are always written by edge id
+    const bool full = pieces == 1 && lo == 0 && hi == g->n_edges;
+    bool any_slabs = false;
+    for (int k = 0; k < dp.ngroups; ++k) any_slabs |= dp.gr[k].slab_of != nullptr;
+    const int32_t *order = !full ? nullptr
+                           : source_order() ? g->eid[1].as<int32_t>()
+                           : (any_slabs && !g->ids_time_ordered) ? g->time_order.as<int32_t>()
+                                                                 : nullptr;
     k_mine_warp<<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
         dg, dpp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt,
         g->split_scratch.as<int32_t>(), (int32_t)split_cap, order);
     TM_LAUNCHED("k_mine_warp");
     if (g->prof && pc == pieces - 1) TM_CUDA(cudaEventRecord(g->ev[1], s));
     for (int r = 0; r < rounds; ++r) {
-      TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int32_t), s));
+      TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(unsigned long long), s));
       k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po,
                                                       g->split_scratch.as<int32_t>(), a, b,
                                                       g->bloom_lists.as<int32_t>());
