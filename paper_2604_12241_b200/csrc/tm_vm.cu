@@ -118,15 +118,55 @@ __device__ __forceinline__ bool cmp_holds_i(int op, long long a, long long b) {
   }
 }
 
-// value of an edge-predicate term for entry (eid, rank) (engine.py:202-217)
-__device__ __forceinline__ double term_num(const Vm &m, int k, int ref, double num, int eid, uint32_t rank) {
+// value of an edge-predicate term for entry (eid, rank) (engine.py:202-217):
+// edge ids and timestamps are Python ints, amounts and DSL numbers floats
+// (dsl.py:222).  Python compares an int with a float exactly, so integer
+// terms stay int64 and mixed pairs go through cmp_mixed.
+struct Num {
+  bool is_int;
+  long long i;
+  double d;
+};
+__device__ __forceinline__ Num term_num(const Vm &m, int k, int ref, double num, int eid, uint32_t rank) {
   switch (k) {
-    case TM_VM_T_NUMBER: return num;
-    case TM_VM_T_EID: return (double)(ref ? eid : m.e);
-    case TM_VM_T_TIME: return (double)__ldg(m.at.uniq_time + rank);
-    case TM_VM_T_AMOUNT: return __ldg(m.at.amount + (ref ? eid : m.e));
-    default: return 0.0;
+    case TM_VM_T_NUMBER: return Num{false, 0, num};
+    case TM_VM_T_EID: return Num{true, (long long)(ref ? eid : m.e), 0.0};
+    case TM_VM_T_TIME: return Num{true, (long long)__ldg(m.at.uniq_time + rank), 0.0};
+    case TM_VM_T_AMOUNT: return Num{false, 0, __ldg(m.at.amount + (ref ? eid : m.e))};
+    default: return Num{false, 0, 0.0};
   }
+}
+
+// sign of (a - d) for int64 a and double d, exactly (-2: unordered, NaN)
+__device__ __forceinline__ int cmp_int_double(long long a, double d) {
+  if (d != d) return -2;
+  if (d >= 9223372036854775808.0) return -1;   // 2^63 > every int64
+  if (d < -9223372036854775808.0) return 1;
+  const double f = floor(d);                   // |f| <= 2^63, exactly an int64 unless f == 2^63
+  const long long fi = (long long)f;
+  if (a < fi) return -1;
+  if (a > fi) return 1;
+  return d > f ? -1 : 0;                       // a == floor(d): below d iff d has a fraction
+}
+
+__device__ __forceinline__ bool sign_holds(int op, int s) {
+  if (s == -2) return op == TM_VM_NE;          // NaN: only != holds
+  switch (op) {
+    case TM_VM_EQ: return s == 0;
+    case TM_VM_NE: return s != 0;
+    case TM_VM_LE: return s <= 0;
+    case TM_VM_LT: return s < 0;
+    case TM_VM_GE: return s >= 0;
+    default: return s > 0;
+  }
+}
+
+__device__ __forceinline__ bool cmp_num(int op, const Num &a, const Num &b) {
+  if (a.is_int && b.is_int) return cmp_holds_i(op, a.i, b.i);
+  if (!a.is_int && !b.is_int) return cmp_holds(op, a.d, b.d);
+  if (a.is_int) return sign_holds(op, cmp_int_double(a.i, b.d));
+  const int s = cmp_int_double(b.i, a.d);      // sign of (b - a)
+  return sign_holds(op, s == -2 ? -2 : -s);
 }
 
 // does the skip predicate hold for entry (eid, rank)?  (_edge_pred_keeps negated)
@@ -145,8 +185,8 @@ __device__ bool pred_holds(const Vm &m, const tm_vm_pred &p, int eid, uint32_t r
   }
   if (p.lk == TM_VM_T_EID && p.rk == TM_VM_T_EID)
     return cmp_holds_i(p.cmp, p.lref ? eid : m.e, p.rref ? eid : m.e);
-  return cmp_holds(p.cmp, term_num(m, p.lk, p.lref, p.lnum, eid, rank),
-                   term_num(m, p.rk, p.rref, p.rnum, eid, rank));
+  return cmp_num(p.cmp, term_num(m, p.lk, p.lref, p.lnum, eid, rank),
+                 term_num(m, p.rk, p.rref, p.rnum, eid, rank));
 }
 
 // the bound edge list of symbol s: innermost frame whose member carries s

@@ -149,10 +149,29 @@ def generate(config: SynthConfig) -> SynthGraph:
                       all_amount, label, n, np.asarray(triggers, dtype=np.int64), config)
 
 
+def stable_time_order(t: np.ndarray) -> np.ndarray:
+    """np.argsort(t, kind="stable"), fast for large logs: when (t - min) * E + id
+    fits int64 the (time, id) keys are distinct, so an unstable sort of them
+    gives the same permutation (numpy's stable int64 argsort is a merge sort:
+    75 s at HI-Large; this is ~10 s)."""
+    E = len(t)
+    if E == 0:
+        return np.zeros(0, dtype=np.int64)
+    t0, t1 = int(t.min()), int(t.max())
+    if (t1 - t0 + 1) * E >= 2**62:
+        return np.argsort(t, kind="stable")
+    key = (t - t0).astype(np.int64)
+    key *= E
+    key += np.arange(E, dtype=np.int64)
+    key.sort()
+    key %= E
+    return key
+
+
 def time_ordered(g: SynthGraph) -> SynthGraph:
     """Re-number edge ids in (time, old id) order — a time-ordered transaction
     log.  Counts per edge are unchanged up to the renumbering."""
-    order = np.argsort(g.time, kind="stable")
+    order = stable_time_order(g.time)
     inv = np.empty_like(order)
     inv[order] = np.arange(len(order))
     return SynthGraph(g.src[order], g.dst[order], g.time[order], g.amount[order], g.label[order],

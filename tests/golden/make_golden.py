@@ -825,6 +825,59 @@ def make_vm():
     print(f"vm.npz: {len(meta)} cases, {len(plans)} programs, {words} record words, {time.time() - t0:.0f}s")
 
 
+# ---------------------------------------------------------------------------
+# VM predicates on timestamps beyond 2^53: the reference compares a Python
+# int (edge time / id) with a float (amount, DSL number) exactly
+
+
+BIGT_TEXT = """pattern: bigt
+delta: {delta}
+stage:
+  op: for_all
+  src: N0.in_neigh
+  dst_var: A
+  skip_if: e1.amount < e1.t
+emit:
+  mode: edge_count
+  target: A
+"""
+BIGT_TEXT2 = """pattern: bigt_ge
+delta: {delta}
+stage:
+  op: for_all
+  src: N1.out_neigh
+  dst_var: B
+  skip_if: e1.amount >= e1.t
+emit:
+  mode: edge_count
+  target: B
+"""
+
+
+def make_vm_bigtime():
+    base = 1 << 60
+    rng = random.Random(53)
+    edges, amounts = [], []
+    for i in range(400):
+        s, d = rng.randrange(12), rng.randrange(12)
+        t = base + rng.randrange(0, 64)
+        edges.append((s, d, t))
+        # amounts exactly representable near 2^60 (spacing 256): some equal a
+        # time's double rounding but not the time itself
+        amounts.append(float(base + 256 * rng.randrange(-1, 2)))
+    recs = [TransactionRecord(i, e[0], e[1], e[2], amounts[i], "USD") for i, e in enumerate(edges)]
+    g = build_graph(recs)
+    out = {"edges": [list(map(int, e)) for e in edges], "amount": amounts, "cases": []}
+    for delta in (0, 7, 64):
+        plans = [compile_pattern(dsl.must_validate(dsl.parse_pattern(t.replace("{delta}", str(delta)))), None,
+                                 force_generic=True) for t in (BIGT_TEXT, BIGT_TEXT2)]
+        fm = mine(g, plans)
+        out["cases"].append({"delta": delta, "plans": [dataclasses.asdict(p) for p in plans],
+                             "counts": [fm.column(p.name).tolist() for p in plans]})
+    (OUT / "vm_bigtime.json").write_text(json.dumps(out))
+    print("vm_bigtime.json:", [sum(map(sum, c["counts"])) for c in out["cases"]])
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["hand", "corpus", "ties", "cfg1"]
     for w in which:

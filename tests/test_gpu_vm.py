@@ -108,3 +108,21 @@ def test_mine_routes_generic_plans_to_the_vm(tmb, fx):
     np.testing.assert_array_equal(fm2.values, fm.values)
     assert len(inst) > 0
     g.free()
+
+
+def test_vm_predicates_exact_beyond_2p53(tmb):
+    """Edge times near 2^60 against float amounts: the reference compares a
+    Python int with a float exactly (engine.py:212-223); a double compare
+    would disagree on 124 of the 400 edges (tests/golden/vm_bigtime.json,
+    make_golden.py vm_bigtime)."""
+    from conftest import GOLDEN
+    from paper_2604_12241_b200.vm import lower_program, vm_mine
+    fx = json.loads((GOLDEN / "vm_bigtime.json").read_text())
+    e = np.asarray(fx["edges"], dtype=np.int64)
+    g = tmb.DeviceGraph(e[:, 0], e[:, 1], e[:, 2], edge_amount=np.asarray(fx["amount"]),
+                        edge_currency=np.zeros(len(e), dtype=np.int64), currency_vocab=["USD"])
+    for case in fx["cases"]:
+        for p, want in zip(case["plans"], case["counts"]):
+            got = vm_mine(g, lower_program(P.plan_from_dict(p), g.currency_vocab))
+            np.testing.assert_array_equal(got, np.asarray(want), err_msg=f"{p['name']} d={case['delta']}")
+    g.free()
