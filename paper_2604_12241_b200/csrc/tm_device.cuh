@@ -64,19 +64,19 @@ struct Ctx {
   int64_t soff = 0;   // slab view: row of the trigger's slab in the offset table
 };
 
-// Both variants measured slower on HI-Small (4.73 -> 5.25 ms/step,
+// Galloping upper bounds measured slower on HI-Small (4.73 -> 5.25 ms/step,
 // tools/sweep_budget.py A/B): kept off, selectable for other graphs.
 #ifndef TM_UB_GALLOP
 #define TM_UB_GALLOP 0
-#endif
-#ifndef TM_FILL_INTERLEAVE
-#define TM_FILL_INTERLEAVE 0
 #endif
 #ifndef TM_SCAN4
 #define TM_SCAN4 1  // measured: HI-Small -4 %, HI-Medium -3 %
 #endif
 #ifndef TM_WIN_PAR
 #define TM_WIN_PAR 1  // measured: HI-Medium -3 %
+#endif
+#ifndef TM_WIN4
+#define TM_WIN4 0  // trigger windows: one joint bisection loop for all four (A/B)
 #endif
 
 
@@ -92,71 +92,125 @@ __device__ __forceinline__ int ub_gallop(const uint32_t *__restrict__ r, int s, 
   return ub_u32(r, lo + 1, min(lo + step, e), x);
 }
 
-// windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
-__device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
-  TM_CNT(kCtrWin, 1);
-  const int32_t *pt = c.g.ptr[dir] + c.soff;
-  const int a = __ldg(pt + x), b = __ldg(pt + x + 1);
+// Runs of at most kShortRun entries can be counted with independent loads of
+// the whole run — one round trip — instead of a bisection (two or three
+// dependent round trips for 2..4 entries).  Measured slower: the extra load
+// instructions cost more than the round trips they save (off by default).
+#ifndef TM_SHORT_RUN
+#define TM_SHORT_RUN 0  // measured: 4 -> HI-Large warp kernel 70.3 -> 89.9 ms, 8 -> 97.6 (more load instructions lose)
+#endif
+constexpr int kShortRun = TM_SHORT_RUN;
+
+// window [lo, hi] (rank space) of the rank-sorted run [a, b) of r
+__device__ __forceinline__ Win window_of_run(const uint32_t *__restrict__ r, int a, int b, uint32_t lo,
+                                             uint32_t hi) {
+  if (b - a <= kShortRun) {
+    int l = a, u = a;
+#pragma unroll
+    for (int k = 0; k < kShortRun; ++k) {
+      if (a + k < b) {
+        const uint32_t x = __ldg(r + a + k);
+        l += x < lo;
+        u += x <= hi;
+      }
+    }
+    return {l, u};
+  }
 #if TM_WIN_PAR
   // both bounds bisected at once: two independent load chains in flight
-  const uint32_t *__restrict__ r = c.g.rnk[dir];
   int l0 = a, l1 = b, u0 = a, u1 = b;
   while (l0 < l1 || u0 < u1) {
     if (l0 < l1) {
       const int m = (l0 + l1) >> 1;
-      if (__ldg(r + m) < c.lo) l0 = m + 1; else l1 = m;
+      if (__ldg(r + m) < lo) l0 = m + 1; else l1 = m;
     }
     if (u0 < u1) {
       const int m = (u0 + u1) >> 1;
-      if (__ldg(r + m) <= c.hi) u0 = m + 1; else u1 = m;
+      if (__ldg(r + m) <= hi) u0 = m + 1; else u1 = m;
     }
   }
   return {l0, u0};
-#endif
-  const int wa = lb_u32(c.g.rnk[dir], a, b, c.lo);
-#if TM_UB_GALLOP
-  return {wa, ub_gallop(c.g.rnk[dir], wa, b, c.hi)};
 #else
-  return {wa, ub_u32(c.g.rnk[dir], wa, b, c.hi)};
+  const int wa = lb_u32(r, a, b, lo);
+#if TM_UB_GALLOP
+  return {wa, ub_gallop(r, wa, b, hi)};
+#else
+  return {wa, ub_u32(r, wa, b, hi)};
+#endif
 #endif
 }
 
+// windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
+__device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
+  TM_CNT(kCtrWin, 1);
+  const int32_t *pt = c.g.ptr[dir] + c.soff;
+  return window_of_run(c.g.rnk[dir], __ldg(pt + x), __ldg(pt + x + 1), c.lo, c.hi);
+}
+
 // trigger windows a delta group needs (bits: 1 u-in, 2 u-out, 4 v-in, 8 v-out).
-// The four lower-bound bisections run interleaved, so their dependent load
-// chains overlap (4 loads in flight per thread instead of 1).
+// All run bounds are loaded first, then every short run in one round of
+// independent loads; only long runs (hubs) bisect.
 __device__ __forceinline__ void fill_windows(Ctx &c, int need) {
-#if !TM_FILL_INTERLEAVE
-  c.wui = c.wuo = c.wvi = c.wvo = Win{0, 0};
-  if (need & 1) c.wui = window(c, 0, c.u);
-  if (need & 2) c.wuo = window(c, 1, c.u);
-  if (need & 4) c.wvi = window(c, 0, c.v);
-  if (need & 8) c.wvo = window(c, 1, c.v);
-#else
-  int a[4], b[4], e[4];
-  const uint32_t *r[4];
+  int a[4], b[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int dir = i & 1, x = (i >> 1) ? c.v : c.u;
-    r[i] = c.g.rnk[dir];
     const bool on = (need >> i) & 1;
-    a[i] = on ? __ldg(c.g.ptr[dir] + c.soff + x) : 0;
-    b[i] = on ? __ldg(c.g.ptr[dir] + c.soff + x + 1) : 0;
-    e[i] = b[i];
+    const int32_t *pt = c.g.ptr[dir] + c.soff;
+    a[i] = on ? __ldg(pt + x) : 0;
+    b[i] = on ? __ldg(pt + x + 1) : 0;
   }
-  while (a[0] < b[0] || a[1] < b[1] || a[2] < b[2] || a[3] < b[3]) {
+  Win w[4];
+#if TM_WIN4
+  // the four windows bisected together: up to 8 independent chains in flight
+  int l0[4], l1[4], u0[4], u1[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) l0[i] = u0[i] = a[i], l1[i] = u1[i] = b[i];
+  bool more = true;
+  while (more) {
+    more = false;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      if (a[i] < b[i]) {
-        const int m = (a[i] + b[i]) >> 1;
-        if (__ldg(r[i] + m) < c.lo) a[i] = m + 1; else b[i] = m;
+      const uint32_t *__restrict__ r = c.g.rnk[i & 1];
+      if (l0[i] < l1[i]) {
+        const int m = (l0[i] + l1[i]) >> 1;
+        if (__ldg(r + m) < c.lo) l0[i] = m + 1; else l1[i] = m;
+        more |= l0[i] < l1[i];
+      }
+      if (u0[i] < u1[i]) {
+        const int m = (u0[i] + u1[i]) >> 1;
+        if (__ldg(r + m) <= c.hi) u0[i] = m + 1; else u1[i] = m;
+        more |= u0[i] < u1[i];
       }
     }
   }
-  c.wui = Win{a[0], ub_gallop(r[0], a[0], e[0], c.hi)};
-  c.wuo = Win{a[1], ub_gallop(r[1], a[1], e[1], c.hi)};
-  c.wvi = Win{a[2], ub_gallop(r[2], a[2], e[2], c.hi)};
-  c.wvo = Win{a[3], ub_gallop(r[3], a[3], e[3], c.hi)};
+  c.wui = Win{l0[0], u0[0]};
+  c.wuo = Win{l0[1], u0[1]};
+  c.wvi = Win{l0[2], u0[2]};
+  c.wvo = Win{l0[3], u0[3]};
+  return;
 #endif
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t *__restrict__ r = c.g.rnk[i & 1];
+    int l = a[i], u = a[i];
+#pragma unroll
+    for (int k = 0; k < kShortRun; ++k) {
+      if (b[i] - a[i] <= kShortRun && a[i] + k < b[i]) {
+        const uint32_t x = __ldg(r + a[i] + k);
+        l += x < c.lo;
+        u += x <= c.hi;
+      }
+    }
+    w[i] = Win{l, u};
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (b[i] - a[i] > kShortRun) w[i] = window_of_run(c.g.rnk[i & 1], a[i], b[i], c.lo, c.hi);
+  c.wui = w[0];
+  c.wuo = w[1];
+  c.wvi = w[2];
+  c.wvo = w[3];
 }
 
 // self-loops of x inside the window (kernels.py:279-287): pair run (x, x);
@@ -249,6 +303,19 @@ __device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Wi
   }
 #endif
   return exists_pair(c, dir, x, __ldg(c.g.gptr[dir] + x), __ldg(c.g.gptr[dir] + x + 1), n);
+}
+
+// n in N^dir(x) for a wide x (a hub, pair-index run [xs, xe)): in a slab
+// view n's opposite window is usually a few L2-resident entries — scan it
+// for x; else one bisection of the shorter pair-index run
+__device__ __forceinline__ bool exists_hub(const Ctx &c, int dir, int x, int xs, int xe, int n) {
+#if TM_SLAB_PROBE
+  if (c.g.ptr[dir ^ 1] != c.g.gptr[dir ^ 1]) {
+    const Win wn = window(c, dir ^ 1, n);
+    if (wn.len() <= kScanWin) return scan_for(c, dir ^ 1, wn, x);
+  }
+#endif
+  return exists_pair(c, dir, x, xs, xe, n);
 }
 
 __device__ __forceinline__ long long warp_sum(long long x) {

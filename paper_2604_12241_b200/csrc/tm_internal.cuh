@@ -203,6 +203,7 @@ struct SlabIndex {
   DevBuf rnk[2];     // rank per slab entry
   DevBuf slab_of;    // uint16 [R]: slab of each rank
   DevBuf bounds;     // uint32 [2][n_slabs + 1]: S_s (first trigger rank), L_s (first halo rank)
+  DevBuf scratch;    // int32 [2][N+1][n_slabs]: owner-major cell tables of the build
   int n_slabs = 0;
   int64_t entries[2] = {0, 0};
 };

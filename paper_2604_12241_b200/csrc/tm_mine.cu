@@ -217,7 +217,7 @@ __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, in
       const int2 sl = slot_np(c, dy, j);
       const int m = sl.x;
       if (m == x || m == y || m == f || !first_of(c, sl)) continue;
-      hits += exists_pair(c, dx, x, xs, xe, m);
+      hits += exists_hub(c, dx, x, xs, xe, m);
     }
     return hits;
   }
@@ -353,7 +353,7 @@ __device__ __forceinline__ bool pull_candidates(const Ctx &c, const CycGroup &cg
   return true;
 }
 
-template <int MAXD, int L, bool PI>
+template <int L, bool PI>
 __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
                                             int (&path)[kMaxChain], int ja, int jb, const int *cand,
                                             CycAcc &acc, const Queue &qu);
@@ -361,32 +361,35 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
 // a_{L+1} = a chosen (all exclusions checked): close at depth L + 1, descend.
 // A wide a: PI (task kernel) expands it backwards in place, or splits it
 // into chain tasks; the warp kernel hands the whole window to a pull task,
-// keeping its walkers lean.
-template <int MAXD, int L, bool PI>
+// keeping its walkers lean.  The deepest level is cg.maxd at run time: one
+// instantiation per level serves every cycle length (code size: the kernels
+// were bound by instruction-cache misses with one tree per maxd).
+template <int L, bool PI>
 __device__ __forceinline__ void chain_pick(const Ctx &c, const CycGroup &cg, int row, int grp,
                                            int (&path)[kMaxChain], int a, CycAcc &acc,
                                            const Queue &qu) {
   TM_CNT(kCtrChain1 + L, 1);
   const Win w = window(c, 1, a);  // a's out-window: closes and descends
   if (cg.mask & (1 << (L + 1))) close_at(cg, L + 1, close_count<L>(c, a, w, path), acc);
-  if constexpr (L + 1 < MAXD) {
+  if constexpr (L + 1 < kMaxChain) {
+    if (L + 1 >= cg.maxd) return;
     path[L] = a;
     int ja = w.a, jb = w.b;
     const int *cand = nullptr;
     int use[kBCap];
     if (w.len() > cg.deep_split) {
       if constexpr (PI) {
-        if (pull_candidates(c, cg, MAXD, L + 2, w, use, ja, jb)) cand = use;
+        if (pull_candidates(c, cg, cg.maxd, L + 2, w, use, ja, jb)) cand = use;
         else if (emit(qu, row, grp, L + 1, path[0], path[1], path[2], path[3], path[4], w.a, w.b)) return;
       } else {
         if (emit_whole(qu, row, grp, (L + 1) | kPullFlag, path, w.a, w.b)) return;
       }
     }
-    chain_level<MAXD, L + 1, PI>(c, cg, row, grp, path, ja, jb, cand, acc, qu);
+    chain_level<L + 1, PI>(c, cg, row, grp, path, ja, jb, cand, acc, qu);
   }
 }
 
-template <int MAXD, int L, bool PI>
+template <int L, bool PI>
 __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, int row, int grp,
                                             int (&path)[kMaxChain], int ja, int jb, const int *cand,
                                             CycAcc &acc, const Queue &qu) {
@@ -401,7 +404,7 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
   bool filter = false;
   if constexpr (PI) {
     if (qu.bloom) {
-      for (int d = L + 1; d <= MAXD; ++d) {
+      for (int d = L + 1; d <= cg.maxd; ++d) {
         if (!(cg.mask & (1 << d))) continue;
         const int k = 1 + d - L;
         if (k - 2 < kBloomLayers && ((qu.bloom->valid >> (k - 2)) & 1)) need |= 1 << (k - 2);
@@ -426,13 +429,13 @@ __device__ __forceinline__ void chain_level(const Ctx &c, const CycGroup &cg, in
     bool dup = false;
 #pragma unroll
     for (int i = 0; i + 1 < L; ++i) dup |= (path[i] == a);
-    if (dup || !(cand ? exists_pair(c, 1, owner, os, oe, a) : first_of(c, sl))) continue;
-    chain_pick<MAXD, L, PI>(c, cg, row, grp, path, a, acc, qu);
+    if (dup || !(cand ? exists_hub(c, 1, owner, os, oe, a) : first_of(c, sl))) continue;
+    chain_pick<L, PI>(c, cg, row, grp, path, a, acc, qu);
   }
 }
 
 // cycles through chain node a1 = m (a V item), depths 1..maxd
-template <int MAXD, bool PI>
+template <bool PI>
 __device__ __forceinline__ void cycles_a1(const Ctx &c, const CycGroup &cg, int row, int grp,
                                           int (&path)[kMaxChain], const Win &w, CycAcc &acc,
                                           const Queue &qu) {
@@ -441,13 +444,13 @@ __device__ __forceinline__ void cycles_a1(const Ctx &c, const CycGroup &cg, int 
   int use[kBCap];
   if (w.len() > cg.deep_split) {
     if constexpr (PI) {
-      if (pull_candidates(c, cg, MAXD, 2, w, use, ja, jb)) cand = use;
+      if (pull_candidates(c, cg, cg.maxd, 2, w, use, ja, jb)) cand = use;
       else if (emit(qu, row, grp, 1, path[0], -1, -1, -1, -1, w.a, w.b)) return;
     } else {
       if (emit_whole(qu, row, grp, 1 | kPullFlag, path, w.a, w.b)) return;
     }
   }
-  chain_level<MAXD, 1, PI>(c, cg, row, grp, path, ja, jb, cand, acc, qu);
+  chain_level<1, PI>(c, cg, row, grp, path, ja, jb, cand, acc, qu);
 }
 
 template <bool PI>
@@ -456,13 +459,7 @@ __device__ __forceinline__ void cycles_from_a1(const Ctx &c, const CycGroup &cg,
   int path[kMaxChain] = {m, -1, -1, -1, -1};
   const Win w = window(c, 1, m);
   if (cg.mask & 2) close_at(cg, 1, close_count<0>(c, m, w, path), acc);
-  switch (cg.maxd) {
-    case 0: case 1: return;
-    case 2: cycles_a1<2, PI>(c, cg, row, grp, path, w, acc, qu); break;
-    case 3: cycles_a1<3, PI>(c, cg, row, grp, path, w, acc, qu); break;
-    case 4: cycles_a1<4, PI>(c, cg, row, grp, path, w, acc, qu); break;
-    default: cycles_a1<5, PI>(c, cg, row, grp, path, w, acc, qu); break;
-  }
+  if (cg.maxd >= 2) cycles_a1<PI>(c, cg, row, grp, path, w, acc, qu);
 }
 
 // a chain task resumes at level L with a1..a_L given (entries [ja, jb) of
@@ -471,15 +468,12 @@ __device__ __forceinline__ void cycles_resume(const Ctx &c, const CycGroup &cg, 
                                               int L, const int (&p0)[kMaxChain], int ja, int jb,
                                               const int *cand, CycAcc &acc, const Queue &qu) {
   int path[kMaxChain] = {p0[0], p0[1], p0[2], p0[3], p0[4]};
-  switch (cg.maxd * 8 + L) {
-#define TM_CHAIN_CASE(D_, L_) \
-  case D_ * 8 + L_: chain_level<D_, L_, true>(c, cg, row, grp, path, ja, jb, cand, acc, qu); return;
-    TM_CHAIN_CASE(2, 1)
-    TM_CHAIN_CASE(3, 1) TM_CHAIN_CASE(3, 2)
-    TM_CHAIN_CASE(4, 1) TM_CHAIN_CASE(4, 2) TM_CHAIN_CASE(4, 3)
-    TM_CHAIN_CASE(5, 1) TM_CHAIN_CASE(5, 2) TM_CHAIN_CASE(5, 3) TM_CHAIN_CASE(5, 4)
-#undef TM_CHAIN_CASE
-    default: return;
+  if (L < 1 || L >= cg.maxd) return;
+  switch (L) {
+    case 1: chain_level<1, true>(c, cg, row, grp, path, ja, jb, cand, acc, qu); return;
+    case 2: chain_level<2, true>(c, cg, row, grp, path, ja, jb, cand, acc, qu); return;
+    case 3: chain_level<3, true>(c, cg, row, grp, path, ja, jb, cand, acc, qu); return;
+    default: chain_level<4, true>(c, cg, row, grp, path, ja, jb, cand, acc, qu); return;
   }
 }
 
@@ -814,7 +808,7 @@ __device__ __forceinline__ bool pull_gs(const Ctx &c, const DevPlans &P, const D
         bool member = false, probed = false;
         for (int gi = 0; gi < gr.n_gs; ++gi) {
           if (hits < P.p[gr.gs_col[gi]].min_size) continue;
-          if (!probed) member = exists_pair(c, 1, c.v, vs, ve, pd[i]), probed = true;
+          if (!probed) member = exists_hub(c, 1, c.v, vs, ve, pd[i]), probed = true;
           if (member) ++cnt[gi];
         }
       }
@@ -965,7 +959,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
         int m;
         if (cand) {
           m = cand[k];
-          if (m == c.u || m == c.v || !exists_pair(c, 1, c.v, vs, ve, m)) continue;
+          if (m == c.u || m == c.v || !exists_hub(c, 1, c.v, vs, ve, m)) continue;
         } else {
           const int2 sl = slot_np(c, 1, k);
           m = sl.x;
@@ -1110,6 +1104,15 @@ static bool own_windows_enabled() {
   return on;
 }
 
+// TM_OWN=2 also builds own-window tables in slab views (A/B)
+static bool own_in_slabs() {
+  static bool on = [] {
+    const char *e = getenv("TM_OWN");
+    return e && e[0] == '2';
+  }();
+  return on;
+}
+
 extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
                        int64_t *out, int out_on_device, void *stream) {
   if (!g) return fail(TM_E_BAD_ARG, "graph is NULL");
@@ -1214,7 +1217,11 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
       dp.gr[k].slab_of = nullptr;
       dp.gr[k].stride = 0;
     }
-    for (int dir = 0; dir < 2 && own_on; ++dir) {
+    // own-window tables: global view only — in a slab view the windows are
+    // short bisections of L2-resident runs, cheaper than the table passes
+    // (HI-Large: 131 vs 145 ms per step, TM_OWN A/B)
+    const bool own_here = own_on && (!dp.gr[k].slab_of || own_in_slabs());
+    for (int dir = 0; dir < 2 && own_here; ++dir) {
       if (!((dp.gr[k].need >> (dir ? 1 : 2)) & 1)) continue;
       int2 *tab = g->own_tabs.as<int2>() + (size_t)rows * own_i++;
       if (dp.gr[k].slab_of) {

@@ -2,7 +2,8 @@
 
     python tools/ab_libs.py hi-small lib_a.so lib_b.so ...
 
-Each library runs in a fresh process (TM_LIB=path): full 14-column set at
+The workload is generated once (/tmp cache); each library runs in a fresh
+process (TM_LIB=path): full 14-column set at
 delta 86400, device-resident output, best of 5 device-timed calls, plus a
 checksum so variants are compared on identical results.
 """
@@ -16,8 +17,8 @@ sys.path.insert(0, ".")
 import numpy as np, torch
 import paper_2604_12241_b200 as tmb
 from paper_2604_12241_b200 import _lib, synth
-g0 = synth.time_ordered(synth.generate(synth.CONFIGS[sys.argv[1]]))
-g = tmb.DeviceGraph(g0.src, g0.dst, g0.time, node_count=g0.node_count)
+z = np.load(sys.argv[3])
+g = tmb.DeviceGraph(z["src"], z["dst"], z["time"], node_count=int(z["n"]))
 _lib.check(_lib.load().tm_set_profiling(g.handle, 1), "prof")
 descs = [tmb.lower_plan(p) for p in tmb.full_pattern_set(86400)]
 E = g.edge_count
@@ -37,6 +38,13 @@ print(json.dumps({"lib": sys.argv[2], "config": sys.argv[1], "ms": round(best[0]
 '''
 
 cfg = sys.argv[1]
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+from paper_2604_12241_b200 import synth  # noqa: E402
+cache = f"/tmp/ab_{cfg}.npz"
+if not os.path.exists(cache):  # generate once for every variant
+    g0 = synth.time_ordered(synth.generate(synth.CONFIGS[cfg]))
+    np.savez(cache, src=g0.src, dst=g0.dst, time=g0.time, n=g0.node_count)
 for lib in sys.argv[2:]:
     env = dict(os.environ, TM_LIB=os.path.abspath(lib))
-    subprocess.run([sys.executable, "-c", CODE, cfg, os.path.basename(lib)], env=env, check=False)
+    subprocess.run([sys.executable, "-c", CODE, cfg, os.path.basename(lib), cache], env=env, check=False)

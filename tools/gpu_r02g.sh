@@ -1,0 +1,7 @@
+# tiled slab fill: parity + HI-Large launch list; register-cap A/B at HI-Large
+set -x
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/r02g_gpu_tests.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02g_launches_hl.csv \
+  python bench.py --config hi-large --steps 1 --warmup 0 --no-e2e --no-parity --no-families > gpurun_out/r02g_launch.log 2>&1
+timeout 1500 python tools/ab_libs.py hi-large ablibs/base.so ablibs/minb20.so ablibs/minb24.so ablibs/minb32.so > gpurun_out/r02g_ab.jsonl 2> gpurun_out/r02g_ab.err
