@@ -298,7 +298,7 @@ def timed_mine(tmb, g, descs, lo, hi, out, stream, flush, steps, warmup, sampler
     flushed before each; returns (step_ms, warp_kernel_ms, launches, clocks)."""
     import torch
     from paper_2604_12241_b200 import _lib
-    step_ms, light_ms = [], []
+    step_ms, light_ms, prep_ms, heavy_ms = [], [], [], []
     launches = 0
     sampler = None
     for step in range(warmup + steps):
@@ -319,8 +319,14 @@ def timed_mine(tmb, g, descs, lo, hi, out, stream, flush, steps, warmup, sampler
             launches += _lib.kernel_launch_count() - c0
             step_ms.append(ev0.elapsed_time(ev1))
             light_ms.append(st.light_ms)
+            prep_ms.append(st.prep_ms)
+            heavy_ms.append(st.heavy_ms)
     clocks = sampler.stop() if sampler else None
+    timed_mine.parts = {"prep_ms": float(np.mean(prep_ms)), "task_kernels_ms": float(np.mean(heavy_ms))}
     return step_ms, light_ms, launches, clocks
+
+
+timed_mine.parts = None
 
 
 def main():
@@ -456,6 +462,9 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "mining step (k_own_windows + k_mine_warp + task rounds)",
                 "step_ms": step_alone_ms, "warp_kernel_ms": lm,
+                "prep_ms": (timed_mine.parts or {}).get("prep_ms"),
+                "task_kernels_ms": (timed_mine.parts or {}).get("task_kernels_ms"),
+                "prep": "per call: rank-window tables + the time-slab view of the dual CSR (tm_slab.cu)",
                 "warp_kernel_share": lm / step_alone_ms if step_alone_ms > 0 else None,
                 "bytes_per_edge": b_edge, "peak_source": peak_src,
                 "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum "

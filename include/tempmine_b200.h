@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define TM_ABI_VERSION 5
+#define TM_ABI_VERSION 6
 
 /* pattern families (plan.py kernel hints + the extended north-star set) */
 enum tm_family {
@@ -110,12 +110,12 @@ typedef struct tm_mine_stats {
                              rows), -1 when not read back (device-output calls) */
   int64_t kernel_launches;/* launches issued by the last tm_mine */
   float light_ms;         /* CUDA-event time (profiling on, else -1) of the
-                             trigger kernel (k_mine_warp), after the call's
-                             window tables */
+                             trigger kernel (k_mine_warp) */
   float heavy_ms;         /* from there to the end of the task rounds and
                              k_mine_finalize (task kernel time) */
   float total_ms;         /* CUDA-event time of the whole call on the device */
-  int32_t reserved;
+  float prep_ms;          /* from the call's start to the trigger kernel:
+                             window-start tables, time-slab views */
 } tm_mine_stats;
 
 int tm_abi_version(void);

@@ -69,7 +69,7 @@ class TmGraphInfo(ctypes.Structure):
                 ("max_in_degree", ctypes.c_int64), ("n_selfloops", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("device", ctypes.c_int32),
                 ("rank_bits", ctypes.c_int32), ("node_bits", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("prep_ms", ctypes.c_float)]
 
 
 TM_FMT_MAX = 48
@@ -95,7 +95,7 @@ class TmMineStats(ctypes.Structure):
     _fields_ = [("triggers", ctypes.c_int64), ("heavy_triggers", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("light_ms", ctypes.c_float),
                 ("heavy_ms", ctypes.c_float), ("total_ms", ctypes.c_float),
-                ("reserved", ctypes.c_int32)]
+                ("prep_ms", ctypes.c_float)]
 
 
 # name -> (restype, argtypes): every symbol include/tempmine_b200.h declares
@@ -136,7 +136,7 @@ SIGNATURES = {
     "tm_last_error": (ctypes.c_char_p, []),
     "tm_graph_free": (None, [_P]),
 }
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 # work counters of -DTM_COUNTERS=1 builds (tm_debug_counters; order of
 # dev::CtrId in csrc/tm_device.cuh)

@@ -72,6 +72,9 @@ struct Ctx {
 #ifndef TM_SCAN4
 #define TM_SCAN4 1  // measured: HI-Small -4 %, HI-Medium -3 %
 #endif
+#ifndef TM_VEC_SCAN
+#define TM_VEC_SCAN 0  // measured: HI-Large warp kernel 70.2 -> 73.6 ms (more bytes per probe)
+#endif
 #ifndef TM_WIN_PAR
 #define TM_WIN_PAR 1  // measured: HI-Medium -3 %
 #endif
@@ -101,9 +104,45 @@ __device__ __forceinline__ int ub_gallop(const uint32_t *__restrict__ r, int s, 
 #endif
 constexpr int kShortRun = TM_SHORT_RUN;
 
+// Runs of at most 4 entries (nearly every run of a slab view) can be counted
+// from the aligned 16-byte block(s) holding them — one or two vector loads,
+// one round trip — instead of a bisection (device buffers are padded, so a
+// block may reach past the array end).  Measured much slower: the kernel is
+// bound by the sectors it moves, and the bisection touches fewer.
+#ifndef TM_VEC_RUN
+#define TM_VEC_RUN 0  // measured: HI-Large warp kernel 70.2 -> 106.3 ms
+#endif
+__device__ __forceinline__ void count_block(const uint4 q, int base, int a, int b, uint32_t lo, uint32_t hi,
+                                            int &l, int &u) {
+  const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = base + k;
+    if (i >= a && i < b) {
+      l += v[k] < lo;
+      u += v[k] <= hi;
+    }
+  }
+}
+
 // window [lo, hi] (rank space) of the rank-sorted run [a, b) of r
 __device__ __forceinline__ Win window_of_run(const uint32_t *__restrict__ r, int a, int b, uint32_t lo,
                                              uint32_t hi) {
+#if TM_VEC_RUN
+  if (b - a <= 4) {
+    int l = a, u = a;
+    if (b > a) {
+      const int a4 = a & ~3;
+      const uint4 q0 = __ldg(reinterpret_cast<const uint4 *>(r + a4));
+      if (b > a4 + 4) {
+        const uint4 q1 = __ldg(reinterpret_cast<const uint4 *>(r + a4 + 4));
+        count_block(q1, a4 + 4, a, b, lo, hi, l, u);
+      }
+      count_block(q0, a4, a, b, lo, hi, l, u);
+    }
+    return {l, u};
+  }
+#endif
   if (b - a <= kShortRun) {
     int l = a, u = a;
 #pragma unroll
@@ -141,10 +180,23 @@ __device__ __forceinline__ Win window_of_run(const uint32_t *__restrict__ r, int
 }
 
 // windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
+#ifndef TM_PTR2
+#define TM_PTR2 0  // run bounds of an even node in one 8-byte load (A/B)
+#endif
+__device__ __forceinline__ int2 run_of(const int32_t *__restrict__ pt, int x) {
+#if TM_PTR2
+  const int2 p = __ldg(reinterpret_cast<const int2 *>(pt + (x & ~1)));
+  if (!(x & 1)) return p;
+  return make_int2(p.y, __ldg(pt + x + 1));
+#else
+  return make_int2(__ldg(pt + x), __ldg(pt + x + 1));
+#endif
+}
+
 __device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
   TM_CNT(kCtrWin, 1);
-  const int32_t *pt = c.g.ptr[dir] + c.soff;
-  return window_of_run(c.g.rnk[dir], __ldg(pt + x), __ldg(pt + x + 1), c.lo, c.hi);
+  const int2 ab = run_of(c.g.ptr[dir] + c.soff, x);
+  return window_of_run(c.g.rnk[dir], ab.x, ab.y, c.lo, c.hi);
 }
 
 // trigger windows a delta group needs (bits: 1 u-in, 2 u-out, 4 v-in, 8 v-out).
@@ -156,9 +208,9 @@ __device__ __forceinline__ void fill_windows(Ctx &c, int need) {
   for (int i = 0; i < 4; ++i) {
     const int dir = i & 1, x = (i >> 1) ? c.v : c.u;
     const bool on = (need >> i) & 1;
-    const int32_t *pt = c.g.ptr[dir] + c.soff;
-    a[i] = on ? __ldg(pt + x) : 0;
-    b[i] = on ? __ldg(pt + x + 1) : 0;
+    const int2 ab = on ? run_of(c.g.ptr[dir] + c.soff, x) : make_int2(0, 0);
+    a[i] = ab.x;
+    b[i] = ab.y;
   }
   Win w[4];
 #if TM_WIN4
@@ -266,7 +318,18 @@ __device__ __forceinline__ bool exists_pair(const Ctx &c, int dir, int x, int xs
 __device__ __forceinline__ bool scan_for(const Ctx &c, int dir, const Win &w, int n) {
   TM_CNT(kCtrScanCall, 1);
   bool hit = false;
-#if TM_SCAN4
+#if TM_VEC_SCAN
+  // two 16-byte loads (four entries) per round trip, from the even-aligned
+  // block holding w.a (device buffers are padded past their end)
+  const int2 *__restrict__ nb = c.g.np[dir];
+  for (int j = w.a & ~1; j < w.b && !hit; j += 4) {
+    TM_CNT(kCtrScanLoad, 1);
+    const int4 p0 = __ldg(reinterpret_cast<const int4 *>(nb + j));
+    const int4 p1 = j + 2 < w.b ? __ldg(reinterpret_cast<const int4 *>(nb + j + 2)) : make_int4(-1, 0, -1, 0);
+    hit = (j >= w.a && p0.x == n) | (j + 1 < w.b && p0.z == n) | (p1.x == n && j + 2 < w.b) |
+          (p1.z == n && j + 3 < w.b);
+  }
+#elif TM_SCAN4
   // four independent loads per round trip (the early exit only every 4)
   const int2 *__restrict__ nb = c.g.np[dir];
   for (int j = w.a; j < w.b && !hit; j += 4) {
@@ -294,7 +357,17 @@ __device__ __forceinline__ bool scan_for(const Ctx &c, int dir, const Win &w, in
 // short: scan them.  A wide w (a hub): in a slab view n's opposite window
 // (x in N^{1-dir}(n)) is a short slab run — scan that; else (or when that is
 // wide too) one bisection of the shorter pair-index run.
-__device__ __forceinline__ bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
+// code-size switches (A/B): the mining kernels stall on instruction fetch;
+// out-of-line copies of the widest helpers shrink the hot code
+#ifndef TM_NOINLINE_PROBE
+#define TM_NOINLINE_PROBE 0
+#endif
+#if TM_NOINLINE_PROBE
+#define TM_PROBE_ATTR __noinline__
+#else
+#define TM_PROBE_ATTR __forceinline__
+#endif
+__device__ TM_PROBE_ATTR bool exists_in(const Ctx &c, int dir, int x, const Win &w, int n) {
   if (w.len() <= kScanWin) return scan_for(c, dir, w, n);
 #if TM_SLAB_PROBE
   if (c.g.ptr[dir ^ 1] != c.g.gptr[dir ^ 1]) {

@@ -171,10 +171,14 @@ __global__ void k_gather_time(const uint32_t *__restrict__ rnk, const int64_t *_
 
 }  // namespace
 
+// every device buffer has kPad spare bytes past its end: the walkers' 16-byte
+// vector loads of a run's aligned block may reach past the last entry
+constexpr size_t kPad = 64;
+
 int DevBuf::ensure_on(size_t n, cudaStream_t s) {
   if (n <= bytes && p) return TM_OK;
   release();
-  cudaError_t e = pool_malloc(&p, n ? n : 16, s);
+  cudaError_t e = pool_malloc(&p, n + kPad, s);
   if (e != cudaSuccess) {
     p = nullptr;
     cudaGetLastError();
@@ -197,7 +201,7 @@ int DevBuf::ensure_pooled(size_t n, cudaStream_t s, cudaStream_t free_stream) {
     cudaStreamSynchronize(free_stream);
     release();
   }
-  cudaError_t e = pool_malloc(&p, n ? n : 16, s);
+  cudaError_t e = pool_malloc(&p, n + kPad, s);
   if (e != cudaSuccess) {
     p = nullptr;
     cudaGetLastError();
@@ -214,7 +218,7 @@ int DevBuf::ensure_pooled(size_t n, cudaStream_t s, cudaStream_t free_stream) {
 int DevBuf::ensure(size_t n) {
   if (n <= bytes && p) return TM_OK;
   release();
-  cudaError_t e = cudaMalloc(&p, n ? n : 16);
+  cudaError_t e = cudaMalloc(&p, n + kPad);
   if (e != cudaSuccess) {
     p = nullptr;
     cudaGetLastError();
@@ -547,7 +551,7 @@ extern "C" void tm_graph_free(tm_graph *g) {
   cudaStreamSynchronize(g->stream);
   bool own = g->owns_stream;
   cudaStream_t s = g->stream;
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 4; ++i)
     if (g->ev[i]) cudaEventDestroy(g->ev[i]);
   for (cudaEvent_t e : g->piece_ev)
     if (e) cudaEventDestroy(e);

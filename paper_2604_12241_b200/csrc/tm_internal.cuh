@@ -249,7 +249,7 @@ struct tm_graph {
   int64_t lo_tab_cap = 0;
   tm_mine_stats last{};
   bool prof = false, prof_pending = false;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // warp start, warp end, end, call start
   // host-output pieces: D2H of piece i overlaps mining of piece i+1
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t piece_ev[8] = {};

@@ -200,7 +200,15 @@ __device__ bool emit_whole(const Queue &qu, int row, int grp, int level, const i
 // A wide run of x (a sender hub) is not bisected when y's window is short:
 // y's side is walked and each node probed in the pair index instead.
 constexpr int kLazyRun = 32;
-__device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, int dy,
+#ifndef TM_NOINLINE_INNER
+#define TM_NOINLINE_INNER 0
+#endif
+#if TM_NOINLINE_INNER
+#define TM_INNER_ATTR __noinline__
+#else
+#define TM_INNER_ATTR __forceinline__
+#endif
+__device__ TM_INNER_ATTR int inner_hits(const Ctx &c, int x, int dx, int y, int dy,
                                           const Win &wy, int K, int f) {
   int hits = f >= 0 ? 1 : 0;
   TM_CNT(kCtrInnerCall, 1);
@@ -209,7 +217,8 @@ __device__ __forceinline__ int inner_hits(const Ctx &c, int x, int dx, int y, in
     return hits;
   }
   const int32_t *pt = c.g.ptr[dx] + c.soff;  // x's run (slab view: its slab run)
-  const int xa = __ldg(pt + x), xb = __ldg(pt + x + 1);
+  const int2 xr = run_of(pt, x);
+  const int xa = xr.x, xb = xr.y;
   if (xb - xa > kLazyRun && wy.len() <= kLazyRun) {
     const int xs = __ldg(c.g.gptr[dx] + x), xe = __ldg(c.g.gptr[dx] + x + 1);  // pair-index run
     for (int j = wy.a; j < wy.b && hits < K; ++j) {
@@ -1137,7 +1146,7 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   g->last = tm_mine_stats{};
   g->prof_pending = false;
   g->last.triggers = rows;
-  g->last.light_ms = g->last.heavy_ms = g->last.total_ms = -1.f;
+  g->last.light_ms = g->last.heavy_ms = g->last.total_ms = g->last.prep_ms = -1.f;
   if (rows == 0 || n_plans == 0) return TM_OK;
   TM_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
@@ -1190,6 +1199,7 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   }
   const int64_t R = g->n_ranks;
   int rc;
+  if (g->prof) TM_CUDA(cudaEventRecord(g->ev[3], s));
   if ((rc = g->lo_tabs.ensure_pooled(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * dp.ngroups, s, g->stream))) return rc;
   // own-window tables pay off when a group needs them for many triggers
   const int64_t E = g->n_edges;
@@ -1404,7 +1414,8 @@ extern "C" int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats) {
     TM_CUDA(cudaEventSynchronize(g->ev[2]));
     TM_CUDA(cudaEventElapsedTime(&g->last.light_ms, g->ev[0], g->ev[1]));
     TM_CUDA(cudaEventElapsedTime(&g->last.heavy_ms, g->ev[1], g->ev[2]));
-    TM_CUDA(cudaEventElapsedTime(&g->last.total_ms, g->ev[0], g->ev[2]));
+    TM_CUDA(cudaEventElapsedTime(&g->last.total_ms, g->ev[3], g->ev[2]));
+    TM_CUDA(cudaEventElapsedTime(&g->last.prep_ms, g->ev[3], g->ev[0]));
     g->prof_pending = false;
   }
   *stats = g->last;
@@ -1414,7 +1425,7 @@ extern "C" int tm_last_mine_stats(tm_graph *g, tm_mine_stats *stats) {
 extern "C" int tm_set_profiling(tm_graph *g, int on) {
   if (!g) return fail(TM_E_BAD_ARG, "NULL graph");
   TM_CUDA(cudaSetDevice(g->device));
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 4; ++i)
     if (!g->ev[i]) TM_CUDA(cudaEventCreate(&g->ev[i]));
   g->prof = on != 0;
   return TM_OK;
