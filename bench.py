@@ -3,9 +3,9 @@
 
 One step = one pass of the mining stage over every trigger edge of the
 workload graph (all 14 feature columns for all E edges), graph resident in
-HBM, output int64 (E, 14) in HBM; for N > 1 the edge range is cut into
-interleaved pieces (one sub-range per rank per piece) whose NCCL all-gathers
-overlap the next piece's mining.  `value` = E / max-over-ranks
+HBM, output int64 (E, 14) in HBM; for N > 1 each rank takes a contiguous
+edge range (prepared once per step: its time slabs only), mined in pieces
+whose NCCL all-gathers overlap the next piece's mining.  `value` = E / max-over-ranks
 step time.  Default workload: the north-star HI-Large shape
 (BASELINE.json:north_star, ~180 M transactions) on 1 B200.
 
@@ -349,7 +349,6 @@ def main():
 
     import paper_2604_12241_b200 as tmb
     from paper_2604_12241_b200 import _lib
-    from paper_2604_12241_b200.distributed import INT32_MAX, piece_bounds
 
     w = workload(a.config, rank, world, dist if world > 1 else None)
     plans = tmb.full_pattern_set(DELTA)
@@ -358,7 +357,6 @@ def main():
     C = len(descs)
     E = w.edge_count
     pieces = a.pieces if world > 1 else 1
-    P, sub, pbounds = piece_bounds(E, world, pieces)
     narrow = world > 1 and not a.wide
 
     t0 = time.perf_counter()
@@ -384,16 +382,11 @@ def main():
         total_ms = compute_ms = float(np.sum(step_ms))
         full_out = out
     else:
-        out_pieces = torch.zeros((pieces, sub, C), dtype=torch.int64, device="cuda")
-        out_full = torch.empty((pieces * P, C), dtype=torch.int64, device="cuda")
-        if narrow:
-            n32 = torch.empty((pieces, sub, C), dtype=torch.int32, device="cuda")
-            f32 = torch.empty((pieces * P, C), dtype=torch.int32, device="cuda")
-            flags = torch.zeros((pieces, 1), dtype=torch.int32, device="cuda")
-            flags_all = torch.empty((world, pieces), dtype=torch.int32, device="cuda")
+        from paper_2604_12241_b200.distributed import mine_pipelined
         step_ms, light_ms, mine_ms = [], [], []
         launches = 0
         sampler = None
+        full_out = None
         for step in range(a.warmup + a.steps):
             timed = step >= a.warmup
             if timed and step == a.warmup:
@@ -404,30 +397,16 @@ def main():
             ev0, ev1, evm = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             c0 = _lib.kernel_launch_count()
             ev0.record(stream)
-            works = []
-            for p in range(pieces):
-                plo, phi = pbounds[rank][p]
-                if phi > plo:
-                    tmb.mine_rows_device(g, descs, plo, phi, out_pieces[p].data_ptr(), stream.cuda_stream)
-                dst = out_full[p * P:(p + 1) * P]
-                if narrow:  # int32 transport, overflow flag per piece (distributed.py)
-                    flags[p, 0] = (out_pieces[p].max() > INT32_MAX).to(torch.int32)
-                    n32[p].copy_(out_pieces[p])
-                    works.append(dist.all_gather_into_tensor(f32[p * P:(p + 1) * P], n32[p], async_op=True))
-                else:  # NCCL waits for this stream, then gathers while the next piece is mined
-                    works.append(dist.all_gather_into_tensor(dst, out_pieces[p], async_op=True))
-            evm.record(stream)  # all pieces mined (gathers may still run)
-            for wk in works:
-                wk.wait()
-            if narrow:
-                dist.all_gather_into_tensor(flags_all.view(-1), flags.view(-1))
-                bad = flags_all.amax(dim=0).cpu().numpy()
-                for p in range(pieces):
-                    dst = out_full[p * P:(p + 1) * P]
-                    if bad[p]:
-                        dist.all_gather_into_tensor(dst, out_pieces[p])
-                    else:
-                        dst.copy_(f32[p * P:(p + 1) * P])
+            # one step: prepare this rank's window tables / slab views (its
+            # contiguous trigger range), mine its pieces, gather each piece
+            # while the next is mined, reorder into the final rows
+            full_out = mine_pipelined(
+                E, C, rank, world,
+                lambda lo, hi, o: tmb.mine_rows_device(g, descs, lo, hi, o.data_ptr(), stream.cuda_stream),
+                pieces=pieces, device="cuda", narrow=narrow,
+                prepare=lambda lo, hi: tmb.prepare_views(g, descs, lo, hi, stream.cuda_stream),
+                on_mined=lambda: evm.record(stream))
+            tmb.release_views(g)
             ev1.record(stream)
             ev1.synchronize()
             st = tmb.last_stats(g)
@@ -441,7 +420,6 @@ def main():
         t = torch.tensor([float(np.sum(step_ms)), float(np.sum(mine_ms))], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, compute_ms = float(t[0].item()), float(t[1].item())
-        full_out = out_full[:E]
     ms_per_step = total_ms / a.steps
     value = E / (ms_per_step / 1e3)
 
@@ -578,7 +556,8 @@ def main():
             "data": "synthetic (reference synth model: power-law sources, uniform dst/time, planted "
                     "instances; edge ids time-ordered)",
             "config": dict(workload_config(a.config, w, C),
-                           parallelism=(f"edge ranges x{world}, {pieces} interleaved pieces, NCCL all-gather "
+                           parallelism=(f"contiguous edge range per rank (its slabs prepared once per step), "
+                                        f"{pieces} pieces, NCCL all-gather "
                                         f"({'int32 + overflow flags' if narrow else 'int64'}) per piece "
                                         f"overlapped with mining" if world > 1 else "1 GPU"),
                            graph_build_s=build_s, graph_device_gib=info.device_bytes / 2**30),

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define TM_ABI_VERSION 6
+#define TM_ABI_VERSION 7
 
 /* pattern families (plan.py kernel hints + the extended north-star set) */
 enum tm_family {
@@ -147,6 +147,19 @@ int tm_graph_degrees(const tm_graph *g, int dir, int64_t *deg);
  *                    without synchronizing. */
 int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
             int64_t *out, int out_on_device, void *stream);
+
+/* Build the window-start tables and time-slab views of the plans' deltas for
+ * triggers [lo, hi) once and keep them on the graph: tm_mine calls on
+ * sub-ranges of [lo, hi) with those deltas reuse them instead of building
+ * their own per call.  With edge ids in time order only the slabs holding
+ * [lo, hi) are built (a multi-GPU rank's share; one host sync).  Replaces
+ * any earlier preparation.  Replaces: the per-worker setup of the
+ * reference's fork pool (engine.py:677-690), which shares one TemporalGraph. */
+int tm_mine_prepare(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
+                    void *stream);
+
+/* Forget the prepared tables (their device memory stays with the graph). */
+int tm_mine_release(tm_graph *g);
 
 /* Stats of the last tm_mine; with profiling on this waits for that call's
  * kernels to finish and fills the event timings. */

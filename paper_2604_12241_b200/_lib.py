@@ -110,6 +110,9 @@ SIGNATURES = {
     "tm_graph_degrees": (ctypes.c_int, [_P, ctypes.c_int, _P]),
     "tm_mine": (ctypes.c_int, [_P, ctypes.POINTER(TmPlanDesc), ctypes.c_int, ctypes.c_int64,
                                ctypes.c_int64, _P, ctypes.c_int, _P]),
+    "tm_mine_prepare": (ctypes.c_int, [_P, ctypes.POINTER(TmPlanDesc), ctypes.c_int, ctypes.c_int64,
+                                       ctypes.c_int64, _P]),
+    "tm_mine_release": (ctypes.c_int, [_P]),
     "tm_mine_members": (ctypes.c_int, [_P, ctypes.POINTER(TmPlanDesc), ctypes.c_int, ctypes.c_int64,
                                        ctypes.c_int64, _P, ctypes.c_int, _P]),
     "tm_last_mine_stats": (ctypes.c_int, [_P, ctypes.POINTER(TmMineStats)]),
@@ -136,7 +139,7 @@ SIGNATURES = {
     "tm_last_error": (ctypes.c_char_p, []),
     "tm_graph_free": (None, [_P]),
 }
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 # work counters of -DTM_COUNTERS=1 builds (tm_debug_counters; order of
 # dev::CtrId in csrc/tm_device.cuh)

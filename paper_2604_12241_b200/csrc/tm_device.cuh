@@ -180,17 +180,10 @@ __device__ __forceinline__ Win window_of_run(const uint32_t *__restrict__ r, int
 }
 
 // windowed slice of x's dir-run: rank in [lo, hi]   (kernels.py:268-276)
-#ifndef TM_PTR2
-#define TM_PTR2 0  // run bounds of an even node in one 8-byte load (A/B)
-#endif
+// run [ptr[x], ptr[x+1]) of node x (two loads of one sector; an 8-byte load
+// of even nodes' pairs would need even slab-row offsets)
 __device__ __forceinline__ int2 run_of(const int32_t *__restrict__ pt, int x) {
-#if TM_PTR2
-  const int2 p = __ldg(reinterpret_cast<const int2 *>(pt + (x & ~1)));
-  if (!(x & 1)) return p;
-  return make_int2(p.y, __ldg(pt + x + 1));
-#else
   return make_int2(__ldg(pt + x), __ldg(pt + x + 1));
-#endif
 }
 
 __device__ __forceinline__ Win window(const Ctx &c, int dir, int x) {
@@ -357,8 +350,9 @@ __device__ __forceinline__ bool scan_for(const Ctx &c, int dir, const Win &w, in
 // short: scan them.  A wide w (a hub): in a slab view n's opposite window
 // (x in N^{1-dir}(n)) is a short slab run — scan that; else (or when that is
 // wide too) one bisection of the shorter pair-index run.
-// code-size switches (A/B): the mining kernels stall on instruction fetch;
-// out-of-line copies of the widest helpers shrink the hot code
+// code-size switches (A/B): out-of-line copies of the widest helpers shrink
+// the hot code (the kernels show instruction-fetch stalls), but measured
+// slower — inner_hits out of line: HI-Large warp kernel 70.1 -> 90.8 ms
 #ifndef TM_NOINLINE_PROBE
 #define TM_NOINLINE_PROBE 0
 #endif

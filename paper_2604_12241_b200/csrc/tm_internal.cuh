@@ -205,7 +205,23 @@ struct SlabIndex {
   DevBuf bounds;     // uint32 [2][n_slabs + 1]: S_s (first trigger rank), L_s (first halo rank)
   DevBuf scratch;    // int32 [2][N+1][n_slabs]: owner-major cell tables of the build
   int n_slabs = 0;
+  int s0 = 0;  // first slab built (start / ptr rows are slabs s0..)
   int64_t entries[2] = {0, 0};
+};
+
+// window-start tables and slab views prepared for a trigger range and kept
+// on the graph (tm_mine_prepare): tm_mine calls on sub-ranges with these
+// deltas reuse them instead of building their own
+struct PreparedViews {
+  bool valid = false;
+  int n = 0;
+  int64_t lo = 0, hi = 0;
+  int64_t delta[kMaxGroups] = {};
+  DevBuf lo_tabs;  // [n][R]
+  SlabIndex slabs[kMaxGroups];
+  DevGraph view[kMaxGroups] = {};
+  const uint16_t *slab_of[kMaxGroups] = {};
+  int64_t stride[kMaxGroups] = {};
 };
 
 inline int bits_for(uint64_t maxval) {  // bits to represent [0, maxval]
@@ -255,6 +271,7 @@ struct tm_graph {
   cudaEvent_t piece_ev[8] = {};
   tmb::DevBuf split_counts;
   tmb::SlabIndex slabs[tmb::kMaxGroups];
+  tmb::PreparedViews prep;  // tm_mine_prepare
   int64_t t_min = 0;   // smallest timestamp (ticks)
   tmb::DevBuf time_order;         // int32[E]: edge ids sorted by (time, id)
   bool ids_time_ordered = false;  // time_order is the identity
@@ -276,10 +293,12 @@ struct tm_graph {
 };
 
 namespace tmb {
-// The slab view of delta group k for this call: builds the slab index of
-// `delta` into g->slabs[k] on stream s and fills *view / *slab_of / *stride
-// (the global view when the horizon holds fewer than kMinSlabs windows).
-// lo_tab is the group's rank -> window-start table.
-int build_slab_view(tm_graph *g, int k, int64_t delta, const uint32_t *lo_tab, cudaStream_t s,
-                    DevGraph *view, const uint16_t **slab_of, int64_t *stride);
+// The slab view of `delta`: builds the slab index into si on stream s and
+// fills *view / *slab_of / *stride (the global view when the horizon holds
+// fewer than kMinSlabs windows).  lo_tab is the rank -> window-start table.
+// restrict_range: only the slabs of triggers [trig_lo, trig_hi) (edge ids in
+// time order; one host sync), else every slab.
+int build_slab_view(tm_graph *g, SlabIndex &si, int64_t delta, const uint32_t *lo_tab, cudaStream_t s,
+                    int64_t trig_lo, int64_t trig_hi, bool restrict_range, DevGraph *view,
+                    const uint16_t **slab_of, int64_t *stride);
 }  // namespace tmb

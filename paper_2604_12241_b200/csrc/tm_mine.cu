@@ -492,9 +492,16 @@ __device__ __forceinline__ void cycles_resume(const Ctx &c, const CycGroup &cg, 
 //   col(ci, v)  additive column value      sa() / sc()  stack a / c     c3()  cycle_3 raw
 
 template <class Sink>
+__device__ __forceinline__ void u_item_sl(const Ctx &c, const DevPlans &P, const DevGroup &gr, const int2 sl,
+                                          Sink &sk);
+template <class Sink>
 __device__ __forceinline__ void u_item(const Ctx &c, const DevPlans &P, const DevGroup &gr, int j,
                                        Sink &sk) {
-  const int2 sl = slot_np(c, 0, j);
+  u_item_sl(c, P, gr, slot_np(c, 0, j), sk);
+}
+template <class Sink>
+__device__ __forceinline__ void u_item_sl(const Ctx &c, const DevPlans &P, const DevGroup &gr, const int2 sl,
+                                          Sink &sk) {
   const int m = sl.x;
   TM_CNT(kCtrUWalk, 1);
   if (m == c.u || m == c.v || !first_of(c, sl)) return;
@@ -878,6 +885,44 @@ __device__ void build_bloom(const Ctx &c, TaskBloom &B, int lane, int top, int *
   }
 }
 
+// ---------------------------------------------------------------- TMA staging
+// TM_TMA_TASKS=1 (A/B of the north star's "shared-memory staging of hub
+// adjacency"): a domain task's piece of the hub window (<= kTaskSpan (nbr,
+// prev) entries) is brought into the warp's shared buffer by one
+// cp.async.bulk (TMA bulk copy, mbarrier completion) issued by lane 0, and
+// the lanes walk it from shared memory instead of one coalesced global load
+// per 32 entries.
+#ifndef TM_TMA_TASKS
+#define TM_TMA_TASKS 0
+#endif
+constexpr int kStageEntries = kTaskSpan + 2;  // + even alignment of the start
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+// lane 0: arm the barrier with the byte count and start the bulk copy
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // earlier generic reads of dst
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TM_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TM_WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // Task kinds (one warp per task):
 //   kLvlDomU / kLvlDomV   a piece of a trigger's U / V slice, lane per entry
 //   kLvlPullV             a hub v's whole N+(v): gs from u's side (pull_gs),
@@ -897,6 +942,15 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
   const int lane = threadIdx.x & 31;
   __shared__ TaskBloom blooms[kTaskThreads / 32];
   TaskBloom &bloom = blooms[threadIdx.x >> 5];
+#if TM_TMA_TASKS
+  __shared__ __align__(128) int2 stage_np[kTaskThreads / 32][kStageEntries];
+  __shared__ __align__(8) uint64_t stage_bar[kTaskThreads / 32];
+  int2 *sbuf = stage_np[threadIdx.x >> 5];
+  uint64_t *sbar = &stage_bar[threadIdx.x >> 5];
+  uint32_t sphase = 0;
+  if (lane == 0) mbar_init(sbar);
+  __syncwarp();
+#endif
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int *blist0 = bloom_lists + (size_t)gwarp * 2 * kBloomList, *blist1 = blist0 + kBloomList;
   for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
@@ -921,7 +975,17 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     int use[kBCap];
     if (t.level == kLvlDomU) {
       GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
+#if TM_TMA_TASKS
+      const int a2 = t.a & ~1;
+      __syncwarp();  // every lane is done with the previous piece
+      if (lane == 0)
+        bulk_load(sbuf, c.g.np[0] + a2, (uint32_t)(((t.b - a2) * 8 + 15) & ~15), sbar);
+      mbar_wait(sbar, sphase);
+      sphase ^= 1;
+      for (int j = t.a + lane; j < t.b; j += 32) u_item_sl(c, P, gr, sbuf[j - a2], sk);
+#else
       for (int j = t.a + lane; j < t.b; j += 32) u_item(c, P, gr, j, sk);
+#endif
     } else if (t.level == kLvlDomV || t.level == kLvlPullV) {
       GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
       int parts = t.pad0, ja = t.a, jb = t.b;
@@ -964,13 +1028,27 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
         }
         if (!parts) ja = jb = 0;
       }
+#if TM_TMA_TASKS
+      const int a2 = ja & ~1;
+      const bool staged = !cand && jb > ja && jb - a2 <= kStageEntries;
+      if (staged) {
+        __syncwarp();
+        if (lane == 0) bulk_load(sbuf, c.g.np[1] + a2, (uint32_t)(((jb - a2) * 8 + 15) & ~15), sbar);
+        mbar_wait(sbar, sphase);
+        sphase ^= 1;
+      }
+#endif
       for (int k = ja + lane; k < jb; k += 32) {
         int m;
         if (cand) {
           m = cand[k];
           if (m == c.u || m == c.v || !exists_hub(c, 1, c.v, vs, ve, m)) continue;
         } else {
+#if TM_TMA_TASKS
+          const int2 sl = staged ? sbuf[k - a2] : slot_np(c, 1, k);
+#else
           const int2 sl = slot_np(c, 1, k);
+#endif
           m = sl.x;
           if (m == c.u || m == c.v || !first_of(c, sl)) continue;
         }
@@ -1211,16 +1289,30 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   const DevGraph dg = g->dev();
   int rounds = 0;
   int own_i = 0;
+  const PreparedViews &pv = g->prep;
+  const bool prepared = pv.valid && lo >= pv.lo && hi <= pv.hi;
   for (int k = 0; k < dp.ngroups; ++k) {
-    dp.gr[k].lo_tab = g->lo_tabs.as<uint32_t>() + (size_t)k * R;
-    k_lo_table<<<grid_for(R, 256), 256, 0, s>>>(g->uniq_time.as<int64_t>(), R, deltas[k],
-                                                g->lo_tabs.as<uint32_t>() + (size_t)k * R);
-    TM_LAUNCHED("k_lo_table");
+    int pi = -1;  // the prepared tables of this delta (tm_mine_prepare), if any
+    for (int i = 0; prepared && i < pv.n; ++i)
+      if (pv.delta[i] == deltas[k]) pi = i;
+    if (pi >= 0) {
+      dp.gr[k].lo_tab = pv.lo_tabs.as<uint32_t>() + (size_t)pi * R;
+      dp.gr[k].view = pv.view[pi];
+      dp.gr[k].slab_of = pv.slab_of[pi];
+      dp.gr[k].stride = pv.stride[pi];
+    } else {
+      dp.gr[k].lo_tab = g->lo_tabs.as<uint32_t>() + (size_t)k * R;
+      k_lo_table<<<grid_for(R, 256), 256, 0, s>>>(g->uniq_time.as<int64_t>(), R, deltas[k],
+                                                  g->lo_tabs.as<uint32_t>() + (size_t)k * R);
+      TM_LAUNCHED("k_lo_table");
+    }
     // the group's view of the graph: time slabs when the call covers a good
     // share of the edges (the view costs O(E + n_slabs N) to build)
-    if (rows * 16 >= E) {
-      if ((rc = build_slab_view(g, k, deltas[k], dp.gr[k].lo_tab, s, &dp.gr[k].view, &dp.gr[k].slab_of,
-                                &dp.gr[k].stride)))
+    if (pi >= 0) {
+      // prepared
+    } else if (rows * 16 >= E) {
+      if ((rc = build_slab_view(g, g->slabs[k], deltas[k], dp.gr[k].lo_tab, s, lo, hi, false, &dp.gr[k].view,
+                                &dp.gr[k].slab_of, &dp.gr[k].stride)))
         return rc;
     } else {
       dp.gr[k].view = dg;
@@ -1236,9 +1328,10 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
       int2 *tab = g->own_tabs.as<int2>() + (size_t)rows * own_i++;
       if (dp.gr[k].slab_of) {
         const DevGraph &v = dp.gr[k].view;
-        k_own_windows_slab<<<grid_for(E, 256), 256, 0, s>>>(dg, dp.gr[k].lo_tab, dir, lo, hi, dp.gr[k].slab_of,
-                                                            dp.gr[k].stride, g->slabs[k].start[dir].as<int32_t>(),
-                                                            v.ptr[dir], v.rnk[dir], tab);
+        const SlabIndex &si = pi >= 0 ? pv.slabs[pi] : g->slabs[k];
+        k_own_windows_slab<<<grid_for(E, 256), 256, 0, s>>>(
+            dg, dp.gr[k].lo_tab, dir, lo, hi, dp.gr[k].slab_of, dp.gr[k].stride,
+            si.start[dir].as<int32_t>() - (int64_t)si.s0 * dp.gr[k].stride, v.ptr[dir], v.rnk[dir], tab);
         TM_LAUNCHED("k_own_windows_slab");
       } else {
         k_own_windows<<<grid_for(E, 256), 256, 0, s>>>(dg, dp.gr[k].lo_tab, dir, lo, hi, tab);
@@ -1386,6 +1479,60 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   }
   TM_CUDA(g->end(s));
   g->last.kernel_launches = tm_kernel_launch_count() - launches0;
+  return TM_OK;
+}
+
+// Window-start tables and time-slab views of the plans' deltas, built for
+// triggers [lo, hi) and kept on the graph: tm_mine calls on sub-ranges of
+// [lo, hi) reuse them (the pieces of a multi-GPU step: each rank prepares its
+// own trigger range once per step, and only the slabs those triggers read).
+extern "C" int tm_mine_prepare(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
+                               void *stream) {
+  if (!g) return fail(TM_E_BAD_ARG, "graph is NULL");
+  if (n_plans < 0 || n_plans > kMaxPlans || (n_plans > 0 && !plans))
+    return fail(TM_E_BAD_ARG, "bad plans");
+  if (lo < 0 || hi < lo || hi > g->n_edges) return fail(TM_E_BAD_ARG, "bad trigger range");
+  TM_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  TM_CUDA(g->begin(s));
+  PreparedViews &pv = g->prep;
+  pv.valid = false;
+  pv.n = 0;
+  for (int i = 0; i < n_plans; ++i) {
+    if (plans[i].delta < 0) return fail(TM_E_BAD_ARG, "negative delta");
+    bool seen = false;
+    for (int k = 0; k < pv.n; ++k) seen |= pv.delta[k] == plans[i].delta;
+    if (seen) continue;
+    if (pv.n == kMaxGroups) return fail(TM_E_UNSUPPORTED_PLAN, "more than 8 distinct deltas");
+    pv.delta[pv.n++] = plans[i].delta;
+  }
+  const int64_t R = g->n_ranks;
+  int rc;
+  if ((rc = pv.lo_tabs.ensure_pooled(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * std::max(pv.n, 1), s,
+                                     g->stream)))
+    return rc;
+  for (int k = 0; k < pv.n; ++k) {
+    uint32_t *lt = pv.lo_tabs.as<uint32_t>() + (size_t)k * R;
+    if (R > 0) {
+      k_lo_table<<<grid_for(R, 256), 256, 0, s>>>(g->uniq_time.as<int64_t>(), R, pv.delta[k], lt);
+      TM_LAUNCHED("k_lo_table");
+    }
+    if ((rc = build_slab_view(g, pv.slabs[k], pv.delta[k], lt, s, lo, hi, true, &pv.view[k], &pv.slab_of[k],
+                              &pv.stride[k])))
+      return rc;
+  }
+  pv.lo = lo;
+  pv.hi = hi;
+  pv.valid = true;
+  TM_CUDA(g->end(s));
+  return TM_OK;
+}
+
+// Drop the prepared tables (their memory stays with the graph for re-use).
+extern "C" int tm_mine_release(tm_graph *g) {
+  if (!g) return fail(TM_E_BAD_ARG, "graph is NULL");
+  g->prep.valid = false;
+  g->prep.n = 0;
   return TM_OK;
 }
 

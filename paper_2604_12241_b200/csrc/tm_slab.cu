@@ -23,16 +23,17 @@
 // Build (streaming passes, no sort — the global runs are already sorted by
 // (owner, rank, eid) and a slab run is a contiguous piece of a global run).
 // The per-cell tables are written and read in owner-major [N+1][n_slabs]
-// layout ("T"), where the slots of one owner touch adjacent cells, and
-// transposed through shared memory to the slab-major [n_slabs][N+1] layout
-// ("S") the scan and the mining kernels use:
+// layout ("T"), where the slots of one owner touch adjacent cells; the
+// slab-major [n_slabs][N+1] offsets ("S") the mining kernels use are
+// produced tile by tile (32 owners x all slabs):
 //   k_slab_bounds     S_s = lower_bound(uniq_time, t0 + s W), L_s = lo_tab[S_s]
 //   k_slab_of         slab of every rank
 //   k_slab_edges      per global CSR slot: the first / last slot of each slab
 //                     run it opens / closes -> startT[x][s], endT[x][s]
-//   k_slab_transpose  lenS = endT - startT, startS = startT (slab-major)
-//   exclusive scan    lenS -> ptrS (slab run offsets)
-//   k_slab_delta      deltaT[x][s] = ptrS - startS (owner-major again)
+//   k_slab_tile_sums  per tile and slab: entries (end - start) -> exclusive
+//                     scan over (slab, tile) = every tile's offset
+//   k_slab_tile_ptrs  per-slab prefix inside the tile -> ptrS, startS
+//                     (slab-major) and deltaT = ptrS - startS (owner-major)
 //   k_slab_fill       per global slot: its copies (nbr, prev, rank) at
 //                     slot + deltaT[x][s] for its (at most two) slabs
 #include <algorithm>
@@ -78,73 +79,92 @@ __global__ void k_slab_of(const uint32_t *__restrict__ S, int n_slabs, int64_t R
 // slab s holds global slot j (rank r) iff L_s <= r < S_{s+1}; the slabs of
 // r are [slab_of(r), ...) while L_s <= r (two at most when W >= delta).
 // Cells are owner-major: cell (x, s) = x * ns + s.
+// Only slabs [s0, s1] are built (a prepared view covers the slabs of one
+// rank's trigger range); cell column of slab s = s - s0, ns = s1 - s0 + 1.
 __global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *__restrict__ rnk,
-                             const int32_t *__restrict__ ptr, int64_t E, int ns,
+                             const int32_t *__restrict__ ptr, int64_t E, int s0, int s1,
                              const uint16_t *__restrict__ slab_of, const uint32_t *__restrict__ S,
                              const uint32_t *__restrict__ L, int32_t *__restrict__ startT,
                              int32_t *__restrict__ endT) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= E) return;
-  const int x = __ldg(owner + j);
   const uint32_t r = __ldg(rnk + j);
+  int s = __ldg(slab_of + r);
+  if (s > s1 || (s < s0 && (s + 1 < s0 || __ldg(L + s0) > r))) return;  // in no built slab
+  const int x = __ldg(owner + j);
   const int a = __ldg(ptr + x), b = __ldg(ptr + x + 1);
   const uint32_t rp = j > a ? __ldg(rnk + j - 1) : 0u;
   const uint32_t rn = j + 1 < b ? __ldg(rnk + j + 1) : 0xffffffffu;
-  int32_t *st = startT + (int64_t)x * ns, *en = endT + (int64_t)x * ns;
-  for (int s = __ldg(slab_of + r); s < ns && __ldg(L + s) <= r; ++s) {
+  const int ns = s1 - s0 + 1;
+  int32_t *st = startT + (int64_t)x * ns - s0, *en = endT + (int64_t)x * ns - s0;
+  for (s = max(s, s0); s <= s1 && __ldg(L + s) <= r; ++s) {
     if (j == a || rp < __ldg(L + s)) st[s] = (int32_t)j;          // opens x's run in slab s
     if (j + 1 == b || rn >= __ldg(S + s + 1)) en[s] = (int32_t)(j + 1);  // closes it
   }
 }
 
-// owner-major [rows][ns] -> slab-major [ns][rows] through a 32 x 32 shared tile:
-// lenS = endT - startT, startS = startT
-constexpr int kTT = 32;
-__global__ void k_slab_transpose(const int32_t *__restrict__ startT, const int32_t *__restrict__ endT,
-                                 int64_t rows, int ns, uint32_t *__restrict__ lenS,
-                                 int32_t *__restrict__ startS) {
-  __shared__ int32_t ts[kTT][kTT + 1], tl[kTT][kTT + 1];
-  const int64_t x0 = (int64_t)blockIdx.x * kTT;
-  const int s0 = blockIdx.y * kTT;
-  for (int i = threadIdx.y; i < kTT; i += blockDim.y) {  // read rows x0 + i, columns s0 + tx
-    const int64_t x = x0 + i;
-    const int s = s0 + threadIdx.x;
-    if (x < rows && s < ns) {
-      const int32_t a = startT[x * ns + s];
-      ts[i][threadIdx.x] = a;
-      tl[i][threadIdx.x] = endT[x * ns + s] - a;
-    }
+// The slab-major offsets ptrS[s][x] = (entries of slabs < s) + (entries of
+// slab s owned by nodes < x) are computed straight from the owner-major
+// start / end tables, tile by tile (32 owners x all slabs, one contiguous
+// block of each table): k_slab_tile_sums sums each slab column of a tile,
+// one exclusive scan over the (slab, tile) sums gives every tile's offset,
+// and k_slab_tile_ptrs runs the per-column prefix inside the tile and
+// writes ptrS / startS (slab-major, through shared memory) and deltaT
+// (owner-major) = ptr - start, the shift of a slot's copy in slab s.
+constexpr int kTX = 32;            // owners per tile
+constexpr int kTileThreads = 256;
+__global__ void __launch_bounds__(kTileThreads) k_slab_tile_sums(const int32_t *__restrict__ startT,
+                                                                 const int32_t *__restrict__ endT, int64_t rows,
+                                                                 int ns, int64_t ntiles,
+                                                                 uint32_t *__restrict__ tsum) {
+  __shared__ uint32_t col[128];
+  for (int i = threadIdx.x; i < ns; i += kTileThreads) col[i] = 0;
+  __syncthreads();
+  const int64_t x0 = (int64_t)blockIdx.x * kTX;
+  const int nr = (int)(rows - x0 < kTX ? rows - x0 : kTX);
+  const int64_t base = x0 * ns;
+  for (int k = threadIdx.x; k < nr * ns; k += kTileThreads) {
+    const int32_t len = endT[base + k] - startT[base + k];
+    if (len) atomicAdd(&col[k % ns], (uint32_t)len);
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < kTT; i += blockDim.y) {  // write rows s0 + i, columns x0 + tx
-    const int s = s0 + i;
-    const int64_t x = x0 + threadIdx.x;
-    if (x < rows && s < ns) {
-      lenS[(int64_t)s * rows + x] = (uint32_t)tl[threadIdx.x][i];
-      startS[(int64_t)s * rows + x] = ts[threadIdx.x][i];
-    }
-  }
+  for (int i = threadIdx.x; i < ns; i += kTileThreads) tsum[(int64_t)i * ntiles + blockIdx.x] = col[i];
 }
 
-// deltaT[x][s] = ptrS[s][x] - startS[s][x]: a slot j of x in slab s lands at j + deltaT
-__global__ void k_slab_delta(const int32_t *__restrict__ ptrS, const int32_t *__restrict__ startS,
-                             int64_t rows, int ns, int32_t *__restrict__ deltaT) {
-  __shared__ int32_t td[kTT][kTT + 1];
-  const int64_t x0 = (int64_t)blockIdx.x * kTT;
-  const int s0 = blockIdx.y * kTT;
-  for (int i = threadIdx.y; i < kTT; i += blockDim.y) {  // read rows s0 + i, columns x0 + tx
-    const int s = s0 + i;
-    const int64_t x = x0 + threadIdx.x;
-    if (x < rows && s < ns) {
-      const int64_t c = (int64_t)s * rows + x;
-      td[i][threadIdx.x] = ptrS[c] - startS[c];
+__global__ void __launch_bounds__(kTileThreads) k_slab_tile_ptrs(
+    const int32_t *__restrict__ startT, const int32_t *__restrict__ endT, int64_t rows, int ns, int64_t ntiles,
+    const uint32_t *__restrict__ toff, int32_t *__restrict__ ptrS, int32_t *__restrict__ startS,
+    int32_t *__restrict__ deltaT) {
+  __shared__ int32_t st[kTX][129], pt[kTX][129];
+  const int64_t x0 = (int64_t)blockIdx.x * kTX;
+  const int nr = (int)(rows - x0 < kTX ? rows - x0 : kTX);
+  const int64_t base = x0 * ns;
+  for (int k = threadIdx.x; k < nr * ns; k += kTileThreads) {  // coalesced block reads
+    const int r = k / ns, c = k - r * ns;
+    const int32_t a = startT[base + k];
+    st[r][c] = a;
+    pt[r][c] = endT[base + k] - a;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ns; c += kTileThreads) {  // per-slab prefix over the tile's owners
+    int32_t run = (int32_t)toff[(int64_t)c * ntiles + blockIdx.x];
+    for (int r = 0; r < nr; ++r) {
+      const int32_t len = pt[r][c];
+      pt[r][c] = run;
+      run += len;
     }
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < kTT; i += blockDim.y) {  // write rows x0 + i, columns s0 + tx
-    const int64_t x = x0 + i;
-    const int s = s0 + threadIdx.x;
-    if (x < rows && s < ns) deltaT[x * ns + s] = td[threadIdx.x][i];
+  for (int k = threadIdx.x; k < nr * ns; k += kTileThreads) {  // owner-major shift, coalesced
+    const int r = k / ns, c = k - r * ns;
+    deltaT[base + k] = pt[r][c] - st[r][c];
+  }
+  for (int k = threadIdx.x; k < kTX * ns; k += kTileThreads) {  // slab-major rows, owners fastest
+    const int c = k / kTX, r = k - c * kTX;
+    if (r < nr) {
+      ptrS[(int64_t)c * rows + x0 + r] = pt[r][c];
+      startS[(int64_t)c * rows + x0 + r] = st[r][c];
+    }
   }
 }
 
@@ -162,8 +182,9 @@ constexpr int kFillItems = 2 * kFillTile;    // at most two copies per slot
 constexpr int kMaxSlabBins = 128;            // kMaxSlabs
 __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
     const int32_t *__restrict__ owner, const uint32_t *__restrict__ rnk, const int2 *__restrict__ np,
-    int64_t E, int ns, const uint16_t *__restrict__ slab_of, const uint32_t *__restrict__ L,
+    int64_t E, int s0, int s1, const uint16_t *__restrict__ slab_of, const uint32_t *__restrict__ L,
     const int32_t *__restrict__ deltaT, int2 *__restrict__ snp, uint32_t *__restrict__ srnk) {
+  const int ns = s1 - s0 + 1;  // bins / cell columns: slab - s0
   extern __shared__ unsigned char fill_smem[];
   int2 *b_np = reinterpret_cast<int2 *>(fill_smem);                       // [kFillItems]
   uint32_t *b_rk = reinterpret_cast<uint32_t *>(b_np + kFillItems);      // [kFillItems]
@@ -180,30 +201,41 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
   // slab's halo, s0 + 1
   int2 e[kFillPer];
   uint32_t r[kFillPer];
-  int s0[kFillPer], d0[kFillPer], d1[kFillPer];
+  int b0[kFillPer], d0[kFillPer], d1[kFillPer];  // bin of the first copy, its / the next bin's destination
 #pragma unroll
   for (int k = 0; k < kFillPer; ++k) {
     const int64_t j = base + k * kFillThreads + threadIdx.x;
-    s0[k] = -1;
+    b0[k] = -1;
     if (j < E) {
-      const int x = __ldg(owner + j);
       r[k] = __ldg(rnk + j);
-      e[k] = __ldg(np + j);
-      const int32_t *dt = deltaT + (int64_t)x * ns;
       const int s = __ldg(slab_of + r[k]);
-      s0[k] = s;
-      d0[k] = (int32_t)(j + __ldg(dt + s));
-      d1[k] = (s + 1 < ns && __ldg(L + s + 1) <= r[k]) ? (int32_t)(j + __ldg(dt + s + 1)) : -1;
+      // copies in slabs s (home) and s + 1 (inside its halo), clipped to [s0, s1]
+      const bool home = s >= s0 && s <= s1;
+      const bool next = s + 1 >= s0 && s + 1 <= s1 && __ldg(L + s + 1) <= r[k];
+      if (home || next) {
+        const int x = __ldg(owner + j);
+        e[k] = __ldg(np + j);
+        const int32_t *dt = deltaT + (int64_t)x * ns - s0;
+        if (home) {
+          b0[k] = s - s0;
+          d0[k] = (int32_t)(j + __ldg(dt + s));
+          d1[k] = next ? (int32_t)(j + __ldg(dt + s + 1)) : -1;
+        } else {  // only the halo copy
+          b0[k] = s + 1 - s0;
+          d0[k] = (int32_t)(j + __ldg(dt + s + 1));
+          d1[k] = -1;
+        }
+      }
     }
   }
 #pragma unroll
   for (int k = 0; k < kFillPer; ++k) {
-    if (s0[k] < 0) continue;
-    atomicAdd(&cnt[s0[k]], 1);
-    atomicMin(&first[s0[k]], d0[k]);
+    if (b0[k] < 0) continue;
+    atomicAdd(&cnt[b0[k]], 1);
+    atomicMin(&first[b0[k]], d0[k]);
     if (d1[k] >= 0) {
-      atomicAdd(&cnt[s0[k] + 1], 1);
-      atomicMin(&first[s0[k] + 1], d1[k]);
+      atomicAdd(&cnt[b0[k] + 1], 1);
+      atomicMin(&first[b0[k] + 1], d1[k]);
     }
   }
   __syncthreads();
@@ -227,13 +259,13 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
   // pass 2: stage every copy at off[s] + (dest - first[s])
 #pragma unroll
   for (int k = 0; k < kFillPer; ++k) {
-    if (s0[k] < 0) continue;
-    int q = off[s0[k]] + (d0[k] - first[s0[k]]);
+    if (b0[k] < 0) continue;
+    int q = off[b0[k]] + (d0[k] - first[b0[k]]);
     b_np[q] = e[k];
     b_rk[q] = r[k];
     b_dst[q] = d0[k];
     if (d1[k] >= 0) {
-      q = off[s0[k] + 1] + (d1[k] - first[s0[k] + 1]);
+      q = off[b0[k] + 1] + (d1[k] - first[b0[k] + 1]);
       b_np[q] = e[k];
       b_rk[q] = r[k];
       b_dst[q] = d1[k];
@@ -251,8 +283,9 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
 
 }  // namespace
 
-int build_slab_view(tm_graph *g, int k, int64_t delta, const uint32_t *lo_tab, cudaStream_t s,
-                    DevGraph *view, const uint16_t **slab_of, int64_t *stride) {
+int build_slab_view(tm_graph *g, SlabIndex &si, int64_t delta, const uint32_t *lo_tab, cudaStream_t s,
+                    int64_t trig_lo, int64_t trig_hi, bool restrict_range, DevGraph *view,
+                    const uint16_t **slab_of, int64_t *stride) {
   *view = g->dev();
   *slab_of = nullptr;
   *stride = 0;
@@ -261,17 +294,19 @@ int build_slab_view(tm_graph *g, int k, int64_t delta, const uint32_t *lo_tab, c
   const int64_t E = g->n_edges, N = g->n_nodes, R = g->n_ranks;
   if (E == 0 || R == 0) return TM_OK;
   const int64_t span = g->t_span + 1;  // ticks covered by the distinct times
-  const int64_t w_min = std::max<int64_t>(delta, 1);
+  // slab width >= delta (an edge then lands in at most two slabs);
+  // TM_SLAB_WMULT=k widens slabs to >= k delta (A/B: fewer cells, larger views)
+  int64_t wmult = 1;
+  if (const char *wm = getenv("TM_SLAB_WMULT")) wmult = std::max<int64_t>(1, atoll(wm));
+  const int64_t w_min = std::max<int64_t>(delta, 1) * wmult;
   int64_t n = span / w_min;
   if (n > kMaxSlabs) n = kMaxSlabs;
   if (n < kMinSlabs) return TM_OK;
   const int n_slabs = (int)n;
   const int64_t W = (span + n_slabs - 1) / n_slabs;  // >= delta
   const int64_t N1 = N + 1;
-  const int64_t cells = (int64_t)n_slabs * N1;
   // entries are addressed by int32 offsets: at most 2 E of them when W >= delta
-  if (2 * E >= (int64_t)INT32_MAX || cells >= (int64_t)INT32_MAX) return TM_OK;
-  SlabIndex &si = g->slabs[k];
+  if (2 * E >= (int64_t)INT32_MAX || (int64_t)n_slabs * N1 >= (int64_t)INT32_MAX) return TM_OK;
   si.n_slabs = n_slabs;
   int rc;
   if ((rc = si.slab_of.ensure_pooled(sizeof(uint16_t) * (size_t)R, s, g->stream)) ||
@@ -283,12 +318,30 @@ int build_slab_view(tm_graph *g, int k, int64_t delta, const uint32_t *lo_tab, c
   TM_LAUNCHED("k_slab_bounds");
   k_slab_of<<<grid_for(R, kB), kB, 0, s>>>(S, n_slabs, R, si.slab_of.as<uint16_t>());
   TM_LAUNCHED("k_slab_of");
+  // slabs built: all, or (a prepared view of time-ordered triggers [trig_lo,
+  // trig_hi)) only those holding them — a rank of a multi-GPU run builds
+  // the ~1/world of the view its triggers read (one host sync)
+  int s0 = 0, s1 = n_slabs - 1;
+  if (restrict_range && g->ids_time_ordered && trig_hi > trig_lo) {
+    uint32_t r01[2];
+    TM_CUDA(cudaMemcpyAsync(&r01[0], g->e_rank.as<uint32_t>() + trig_lo, 4, cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaMemcpyAsync(&r01[1], g->e_rank.as<uint32_t>() + trig_hi - 1, 4, cudaMemcpyDeviceToHost, s));
+    uint16_t sl[2];
+    TM_CUDA(cudaStreamSynchronize(s));  // r01 is needed to address slab_of
+    TM_CUDA(cudaMemcpyAsync(&sl[0], si.slab_of.as<uint16_t>() + r01[0], 2, cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaMemcpyAsync(&sl[1], si.slab_of.as<uint16_t>() + r01[1], 2, cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaStreamSynchronize(s));
+    s0 = sl[0];
+    s1 = sl[1];
+  }
+  const int ns = s1 - s0 + 1;
+  const int64_t cells = (int64_t)ns * N1;
+  si.s0 = s0;
   // owner-major scratch, shared by both directions (stream-ordered)
   if ((rc = si.scratch.ensure_pooled(sizeof(int32_t) * 2 * (size_t)cells, s, g->stream))) return rc;
   int32_t *startT = si.scratch.as<int32_t>(), *endT = startT + cells;
   constexpr int kFillSmem = kFillItems * (sizeof(int2) + 2 * sizeof(int32_t));  // 64 KB
   TM_CUDA(cudaFuncSetAttribute(k_slab_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, kFillSmem));
-  const dim3 tgrid((unsigned)((N1 + kTT - 1) / kTT), (unsigned)((n_slabs + kTT - 1) / kTT)), tblock(kTT, 8);
   for (int d = 0; d < 2; ++d) {
     if ((rc = si.start[d].ensure_pooled(sizeof(int32_t) * (size_t)cells, s, g->stream)) ||
         (rc = si.ptr[d].ensure_pooled(sizeof(int32_t) * (size_t)cells, s, g->stream)))
@@ -297,16 +350,20 @@ int build_slab_view(tm_graph *g, int k, int64_t delta, const uint32_t *lo_tab, c
     // cells of owners without entries in a slab stay 0 - 0 (empty runs)
     TM_CUDA(cudaMemsetAsync(startT, 0, sizeof(int32_t) * 2 * (size_t)cells, s));
     k_slab_edges<<<grid_for(E, kB), kB, 0, s>>>(g->owner[d].as<int32_t>(), g->rnk[d].as<uint32_t>(),
-                                                g->ptr[d].as<int32_t>(), E, n_slabs,
+                                                g->ptr[d].as<int32_t>(), E, s0, s1,
                                                 si.slab_of.as<uint16_t>(), S, L, startT, endT);
     TM_LAUNCHED("k_slab_edges");
-    k_slab_transpose<<<tgrid, tblock, 0, s>>>(startT, endT, N1, n_slabs, reinterpret_cast<uint32_t *>(ptr), startS);
-    TM_LAUNCHED("k_slab_transpose");
-    if ((rc = exclusive_scan_u32(reinterpret_cast<uint32_t *>(ptr), reinterpret_cast<uint32_t *>(ptr), cells, s)))
-      return rc;
-    int32_t *deltaT = startT;  // startT / endT are consumed
-    k_slab_delta<<<tgrid, tblock, 0, s>>>(ptr, startS, N1, n_slabs, deltaT);
-    TM_LAUNCHED("k_slab_delta");
+    const int64_t ntiles = (N1 + kTX - 1) / kTX;
+    uint32_t *tsum = nullptr;
+    TM_CUDA(pool_malloc((void **)&tsum, sizeof(uint32_t) * (size_t)(ntiles * ns), s));
+    k_slab_tile_sums<<<(unsigned)ntiles, kTileThreads, 0, s>>>(startT, endT, N1, ns, ntiles, tsum);
+    TM_LAUNCHED("k_slab_tile_sums");
+    if ((rc = exclusive_scan_u32(tsum, tsum, ntiles * ns, s))) return rc;
+    int32_t *deltaT = startT;  // each tile reads its start / end block before writing it back
+    k_slab_tile_ptrs<<<(unsigned)ntiles, kTileThreads, 0, s>>>(startT, endT, N1, ns, ntiles, tsum, ptr,
+                                                                startS, deltaT);
+    TM_LAUNCHED("k_slab_tile_ptrs");
+    TM_CUDA(cudaFreeAsync(tsum, s));
     // W >= delta: an edge lands in at most two slabs, so 2 E entries bound
     // the view without reading the scan's total back (no host sync)
     si.entries[d] = 2 * E;
@@ -314,10 +371,10 @@ int build_slab_view(tm_graph *g, int k, int64_t delta, const uint32_t *lo_tab, c
         (rc = si.rnk[d].ensure_pooled(sizeof(uint32_t) * (size_t)(2 * E), s, g->stream)))
       return rc;
     k_slab_fill<<<grid_for(E, kFillTile), kFillThreads, kFillSmem, s>>>(g->owner[d].as<int32_t>(), g->rnk[d].as<uint32_t>(),
-                                               g->npk[d].as<int2>(), E, n_slabs, si.slab_of.as<uint16_t>(),
+                                               g->npk[d].as<int2>(), E, s0, s1, si.slab_of.as<uint16_t>(),
                                                L, deltaT, si.np[d].as<int2>(), si.rnk[d].as<uint32_t>());
     TM_LAUNCHED("k_slab_fill");
-    view->ptr[d] = ptr;
+    view->ptr[d] = ptr - (int64_t)s0 * N1;  // rows of slabs s0..s1, addressed by slab * (N + 1)
     view->np[d] = si.np[d].as<int2>();
     view->rnk[d] = si.rnk[d].as<uint32_t>();
     // only the global-CSR helpers may touch these in a slab view

@@ -74,42 +74,62 @@ def mine_sharded(n_edges: int, n_cols: int, rank: int, world: int,
 
 
 def piece_bounds(n_edges: int, world: int, pieces: int) -> tuple[int, int, list[list[tuple[int, int]]]]:
-    """Interleaved piece assignment for a pipelined gather.
+    """Piece assignment for a pipelined gather.
 
-    The trigger range is cut into `pieces` global pieces of P rows (P a
-    multiple of `world`); rank r mines sub-range r of every piece.  The
-    all-gather of piece p then lands exactly on global rows [p*P, (p+1)*P)
-    in order, so each piece's gather can start while the next piece is
-    mined — no reordering pass.  Returns (P, sub = P // world,
-    bounds[rank][piece] = (lo, hi)), ranges clamped to n_edges."""
+    Rank r owns the contiguous trigger range [r*C, (r+1)*C), C = pieces*sub
+    (time-contiguous when edge ids are in time order, so the rank builds
+    only the time slabs its triggers read: tm_mine_prepare), cut into
+    `pieces` sub-ranges of `sub` rows.  Gathering piece p brings every
+    rank's p-th sub-range (P = world*sub rows, rank-major); it is written to
+    rows r*C + p*sub of the result while the next piece is mined.  Returns
+    (P, sub, bounds[rank][piece] = (lo, hi)), ranges clamped to n_edges."""
     if world < 1 or pieces < 1:
         raise ValueError("world and pieces must be >= 1")
     sub = (n_edges + world * pieces - 1) // (world * pieces) if n_edges else 0
     P = sub * world
-    bounds = [[(min(p * P + r * sub, n_edges), min(p * P + (r + 1) * sub, n_edges)) for p in range(pieces)]
+    C = sub * pieces
+    bounds = [[(min(r * C + p * sub, n_edges), min(r * C + (p + 1) * sub, n_edges)) for p in range(pieces)]
               for r in range(world)]
     return P, sub, bounds
 
 
+def rank_range(n_edges: int, world: int, pieces: int, rank: int) -> tuple[int, int]:
+    """The contiguous trigger range of `rank` under piece_bounds."""
+    _, sub, b = piece_bounds(n_edges, world, pieces)
+    return b[rank][0][0], b[rank][-1][1]
+
+
 def mine_pipelined(n_edges: int, n_cols: int, rank: int, world: int,
                    mine_block: Callable[[int, int, object], None], pieces: int = 4, device="cuda", group=None,
-                   narrow: bool = False, stats: dict | None = None):
+                   narrow: bool = False, stats: dict | None = None,
+                   prepare: Callable[[int, int], None] | None = None,
+                   on_mined: Callable[[], None] | None = None):
     """Like mine_sharded, but the gather of each piece is issued (async) as
     soon as the piece is mined, so it overlaps the next piece's mining.
 
+    prepare(lo, hi), if given, runs once for the rank's whole range before
+    its pieces (the per-step window tables / slab views, tm_mine_prepare);
+    on_mined(), if given, runs once every piece is enqueued (bench: the
+    compute-only timing event).
     narrow=True: int32 transport with per-piece overflow flags (module doc);
     `stats` (if given) receives {"pieces_int64": n} — pieces that had to be
     re-gathered at full width."""
     import torch
     P, sub, bounds = piece_bounds(n_edges, world, pieces)
-    full = torch.empty((pieces * P, n_cols), dtype=torch.int64, device=device)
+    full = torch.empty((world * pieces * sub, n_cols), dtype=torch.int64, device=device)
+    # gathered pieces arrive rank-major: piece p of rank r -> rows r*C + p*sub
+    dest = full.view(world, pieces, sub, n_cols)
     local = torch.zeros((pieces, sub, n_cols), dtype=torch.int64, device=device)
     works = []
+    stage = torch.empty((pieces * P, n_cols), dtype=torch.int32 if narrow else torch.int64, device=device)
     if narrow:
-        full32 = torch.empty((pieces * P, n_cols), dtype=torch.int32, device=device)
         flags = torch.zeros((pieces, 1), dtype=torch.int32, device=device)
         flags_all = torch.empty((world, pieces), dtype=torch.int32, device=device)
         narrow_local = torch.empty((pieces, sub, n_cols), dtype=torch.int32, device=device)
+    if prepare is not None:
+        lo0, hi0 = bounds[rank][0][0], bounds[rank][-1][1]
+        if hi0 > lo0:
+            prepare(lo0, hi0)
     for p in range(pieces):
         lo, hi = bounds[rank][p]
         if hi > lo:
@@ -119,22 +139,26 @@ def mine_pipelined(n_edges: int, n_cols: int, rank: int, world: int,
             if sub > 0:
                 flags[p, 0] = (local[p].max() > INT32_MAX).to(torch.int32)
             narrow_local[p].copy_(local[p])  # wraps on overflow; the flag redoes the piece
-            works.append(_all_gather(full32[p * P:(p + 1) * P], narrow_local[p], group, async_op=True))
+            works.append(_all_gather(stage[p * P:(p + 1) * P], narrow_local[p], group, async_op=True))
         else:
-            works.append(_all_gather(full[p * P:(p + 1) * P], local[p], group, async_op=True))
+            works.append(_all_gather(stage[p * P:(p + 1) * P], local[p], group, async_op=True))
+    if on_mined is not None:
+        on_mined()
     for w in works:
         w.wait()
+    bad = np.zeros(pieces, dtype=np.int64)
     if narrow:
         _all_gather(flags_all.view(-1), flags.view(-1), group)  # rank r -> row r
         bad = flags_all.amax(dim=0).cpu().numpy()
-        for p in range(pieces):
-            dst = full[p * P:(p + 1) * P]
-            if bad[p]:
-                _all_gather(dst, local[p], group)
-            else:
-                dst.copy_(full32[p * P:(p + 1) * P])
-        if stats is not None:
-            stats["pieces_int64"] = int(np.count_nonzero(bad))
+    for p in range(pieces):
+        if bad[p]:  # int32 wrapped somewhere in this piece: gather it again at full width
+            wide = torch.empty((P, n_cols), dtype=torch.int64, device=device)
+            _all_gather(wide, local[p], group)
+            dest[:, p].copy_(wide.view(world, sub, n_cols))
+        else:  # reorder (and widen) into the final rows
+            dest[:, p].copy_(stage[p * P:(p + 1) * P].view(world, sub, n_cols))
+    if stats is not None:
+        stats["pieces_int64"] = int(np.count_nonzero(bad))
     return full[:n_edges]
 
 
@@ -168,7 +192,8 @@ def mine_distributed(graph, plans, *, group=None, pieces: int = 4, narrow: bool 
     import torch.distributed as dist
 
     from . import _lib
-    from .engine import FeatureMatrix, _chunks, lower_all, mine_members_device, mine_rows_device
+    from .engine import (FeatureMatrix, _chunks, lower_all, mine_members_device, mine_rows_device, prepare_views,
+                         release_views)
     from .graph import as_device_graph
 
     plans, descs = lower_all(plans)
@@ -193,7 +218,9 @@ def mine_distributed(graph, plans, *, group=None, pieces: int = 4, narrow: bool 
         full = mine_pipelined(E, len(part), rank, world,
                               lambda lo, hi, out, dp=dp: on_side(
                                   lambda ptr, st: mine_rows_device(dg, dp, lo, hi, ptr, st), out),
-                              pieces=pieces, device="cuda", group=group, narrow=narrow)
+                              pieces=pieces, device="cuda", group=group, narrow=narrow,
+                              prepare=lambda lo, hi, dp=dp: prepare_views(dg, dp, lo, hi, side.cuda_stream))
+        release_views(dg)
         values[:, part] = full
     for part in _chunks(memb, _lib.MAX_PLANS):
         dp = [descs[i] for i in part]

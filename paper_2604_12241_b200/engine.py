@@ -221,6 +221,22 @@ def mine_rows_device(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: in
         _lib.check(rc, "tm_mine")
 
 
+def prepare_views(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int, stream: int | None = None) -> None:
+    """Build the window-start tables and time-slab views of `descs`' deltas for
+    triggers [lo, hi) once (tm_mine_prepare): later mining calls on sub-ranges
+    reuse them — e.g. the pieces of one multi-GPU step."""
+    arr = _lib.plan_array([d for d in descs if isinstance(d, PlanDesc)])
+    with dgraph.lock:
+        _lib.check(_lib.load().tm_mine_prepare(dgraph.handle, arr, len(arr), lo, hi,
+                                               ctypes.c_void_p(stream) if stream else None), "tm_mine_prepare")
+
+
+def release_views(dgraph: DeviceGraph) -> None:
+    """Forget the tables of prepare_views (tm_mine_release)."""
+    with dgraph.lock:
+        _lib.check(_lib.load().tm_mine_release(dgraph.handle), "tm_mine_release")
+
+
 def mine_members_device(dgraph: DeviceGraph, descs: list[PlanDesc], lo: int, hi: int, out_ptr: int,
                         stream: int | None = None) -> None:
     """Enqueue members attribution of triggers [lo, hi): contributions are

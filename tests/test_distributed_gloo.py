@@ -33,9 +33,11 @@ def test_piece_bounds_cover_rows_in_order():
         P, sub, b = piece_bounds(n, world, pieces)
         assert P == sub * world
         rows = []
-        for p in range(pieces):  # gathered piece p = rank 0's part, rank 1's part, ...
-            for r in range(world):
+        for r in range(world):  # rank r owns a contiguous range, cut into its pieces in order
+            for p in range(pieces):
                 lo, hi = b[r][p]
+                assert hi - lo <= sub
+                assert lo == min(n, (r * pieces + p) * sub)  # piece p of rank r -> rows r*C + p*sub
                 rows.extend(range(lo, hi))
         assert rows == list(range(n))
 
@@ -74,9 +76,10 @@ def _work(rank, world, port, src, dst, t, names, delta, q):
                             stats=st)
     assert torch.equal(full, narrow) and st["pieces_int64"] == 0
 
-    # a block with counts beyond int32 in one rank's part of piece 1 only:
+    # a block with counts beyond int32 in one rank's part of one piece only:
     # that piece is re-gathered at full width, the others stay narrow
-    target = piece_bounds(len(src), world, 3)[2][1][1]  # rank 1's part of piece 1
+    r1 = piece_bounds(len(src), world, 3)[2][1]  # rank 1's pieces
+    target = r1[1] if r1[1][1] > r1[1][0] else r1[0]
 
     def big_block(lo, hi, out):
         block(lo, hi, out)

@@ -6,6 +6,7 @@ graph; prints one JSON line per (L, delta) with ms and edges/s.
 """
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -24,12 +25,23 @@ ap.add_argument("--deltas", default="3600,21600,86400,259200,604800")
 ap.add_argument("--lengths", default="2,3,4,5,6,7,8")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--budget", type=float, default=20.0, help="seconds per run before longer cycles are skipped")
+ap.add_argument("--parity-blocks", type=int, default=16, help="sampled trigger blocks checked per cell (0: off)")
+ap.add_argument("--parity-block", type=int, default=250, help="triggers per sampled block")
 a = ap.parse_args()
 
 g0 = synth.time_ordered(synth.generate(synth.CONFIGS[a.config]))
 g = tmb.DeviceGraph(g0.src, g0.dst, g0.time, node_count=g0.node_count)
 _lib.check(_lib.load().tm_set_profiling(g.handle, 1), "prof")
 E = g.edge_count
+og = None
+if a.parity_blocks:
+    # the CPU oracle (test infrastructure, pinned to the reference's generic
+    # interpreter for cycle_5..8) on sampled trigger blocks of every cell
+    from oracle.oracle import OracleGraph, column
+    og = OracleGraph(g0.src, g0.dst, g0.time, node_count=g0.node_count)
+    rng = np.random.default_rng(4)
+    blocks = [(int(lo), int(lo) + a.parity_block) for lo in rng.integers(0, E - a.parity_block, a.parity_blocks)]
+    idx = torch.from_numpy(np.concatenate([np.arange(lo, hi) for lo, hi in blocks])).cuda()
 stream = torch.cuda.Stream()
 out = torch.empty((E, 1), dtype=torch.int64, device="cuda")
 # deltas outer, lengths inner: once one length at a delta takes longer than
@@ -55,7 +67,15 @@ for d in [int(x) for x in a.deltas.split(",")]:
             if rep >= reps:
                 break
         total = int(out.sum().item())
-        print(json.dumps({"config": a.config, "cycle_len": L, "delta": d, "ms": best.total_ms,
-                          "warp_ms": best.light_ms, "task_ms": best.heavy_ms,
-                          "edges_per_s": E / (best.total_ms / 1e3), "column_sum": total}), flush=True)
+        rec = {"config": a.config, "cycle_len": L, "delta": d, "ms": best.total_ms,
+               "prep_ms": best.prep_ms, "warp_ms": best.light_ms, "task_ms": best.heavy_ms,
+               "edges_per_s": E / (best.total_ms / 1e3), "column_sum": total}
+        if og is not None:
+            got = out.index_select(0, idx).cpu().numpy()[:, 0]
+            t = time.perf_counter()
+            want = np.concatenate([og.mine([column(f"cycle_{L}", d)], lo, hi, threads=os.cpu_count() or 1)[:, 0]
+                                   for lo, hi in blocks])
+            rec["parity"] = {"rows": int(len(want)), "mismatches": int((got != want).sum()),
+                             "oracle_s": time.perf_counter() - t, "checker": "oracle/tm_oracle.c"}
+        print(json.dumps(rec), flush=True)
         slow = best.total_ms > 1e3 * a.budget
