@@ -194,6 +194,7 @@ int exclusive_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, cudaStream_
 
 constexpr int kMaxSlabs = 128;  // slab offset tables are [n_slabs][N+1]
 constexpr int kMinSlabs = 3;    // fewer slabs than this: the global view is used
+constexpr int kSlabMinRun = 32; // mean run length E/N below this: the global view is used
 
 // one delta's slab index (grow-only device storage, tm_slab.cu)
 struct SlabIndex {

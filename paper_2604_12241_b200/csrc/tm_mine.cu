@@ -1391,6 +1391,13 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   const size_t smem = sizeof(long long) * kThreads * std::max(dp.n_stage, 1);
   if (smem > 48 * 1024)
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // TM_CARVEOUT=pct: preferred shared-memory share of the L1/shared array
+  // for the mining kernels (A/B: the walkers' loads are L1-cached)
+  if (const char *co = getenv("TM_CARVEOUT")) {
+    const int pct = atoi(co);
+    TM_CUDA(cudaFuncSetAttribute(k_mine_warp, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    TM_CUDA(cudaFuncSetAttribute(k_mine_tasks, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  }
   // Host output: mine the range in pieces and copy each finished piece back
   // on a copy stream while the next piece is mined — the D2H of the int64
   // block (8*C bytes per trigger over PCIe) is the largest end-to-end cost.

@@ -89,8 +89,8 @@ __global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= E) return;
   const uint32_t r = __ldg(rnk + j);
+  if (r < __ldg(L + s0) || r >= __ldg(S + s1 + 1)) return;  // in no built slab (no slab_of gather)
   int s = __ldg(slab_of + r);
-  if (s > s1 || (s < s0 && (s + 1 < s0 || __ldg(L + s0) > r))) return;  // in no built slab
   const int x = __ldg(owner + j);
   const int a = __ldg(ptr + x), b = __ldg(ptr + x + 1);
   const uint32_t rp = j > a ? __ldg(rnk + j - 1) : 0u;
@@ -183,7 +183,8 @@ constexpr int kMaxSlabBins = 128;            // kMaxSlabs
 __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
     const int32_t *__restrict__ owner, const uint32_t *__restrict__ rnk, const int2 *__restrict__ np,
     int64_t E, int s0, int s1, const uint16_t *__restrict__ slab_of, const uint32_t *__restrict__ L,
-    const int32_t *__restrict__ deltaT, int2 *__restrict__ snp, uint32_t *__restrict__ srnk) {
+    const uint32_t *__restrict__ S_next, const int32_t *__restrict__ deltaT, int2 *__restrict__ snp,
+    uint32_t *__restrict__ srnk) {
   const int ns = s1 - s0 + 1;  // bins / cell columns: slab - s0
   extern __shared__ unsigned char fill_smem[];
   int2 *b_np = reinterpret_cast<int2 *>(fill_smem);                       // [kFillItems]
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
   }
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kFillTile;
+  const uint32_t r_lo = __ldg(L + s0), r_hi = __ldg(S_next + s1);  // ranks held by slabs s0..s1
   // pass 1: load the thread's slots (kept in registers), per-slab counts and
   // first destinations; a slot's copies: home slab s0 and, inside the next
   // slab's halo, s0 + 1
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
     b0[k] = -1;
     if (j < E) {
       r[k] = __ldg(rnk + j);
+      if (r[k] < r_lo || r[k] >= r_hi) continue;  // in no built slab
       const int s = __ldg(slab_of + r[k]);
       // copies in slabs s (home) and s + 1 (inside its halo), clipped to [s0, s1]
       const bool home = s >= s0 && s <= s1;
@@ -228,6 +231,10 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
       }
     }
   }
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < kFillPer; ++k) any |= b0[k] >= 0;
+  if (!__syncthreads_or(any)) return;  // a tile outside the prepared range
 #pragma unroll
   for (int k = 0; k < kFillPer; ++k) {
     if (b0[k] < 0) continue;
@@ -289,10 +296,17 @@ int build_slab_view(tm_graph *g, SlabIndex &si, int64_t delta, const uint32_t *l
   *view = g->dev();
   *slab_of = nullptr;
   *stride = 0;
-  const char *env = getenv("TM_SLABS");  // TM_SLABS=0: global view (A/B)
+  const char *env = getenv("TM_SLABS");  // TM_SLABS=0 / 1: force the global / slab view (A/B)
   if (env && env[0] == '0') return TM_OK;
+  const bool force = env && env[0] == '1';
   const int64_t E = g->n_edges, N = g->n_nodes, R = g->n_ranks;
   if (E == 0 || R == 0) return TM_OK;
+  // The view pays off when the global runs are long (the bisections and the
+  // L2 footprint it saves grow with the mean run length E/N): measured a
+  // win at the HI-Large shape (E/N = 85: 144 -> 100 ms per call), a loss at
+  // HI-Small / HI-Medium (E/N = 10 / 15: 2.9 -> 3.6, 17.4 -> 19.3 ms) and
+  // at short windows (many slabs: 1-h windows on HI-Medium 1.2 -> 10 ms).
+  if (!force && E < kSlabMinRun * N) return TM_OK;
   const int64_t span = g->t_span + 1;  // ticks covered by the distinct times
   // slab width >= delta (an edge then lands in at most two slabs);
   // TM_SLAB_WMULT=k widens slabs to >= k delta (A/B: fewer cells, larger views)
@@ -305,6 +319,7 @@ int build_slab_view(tm_graph *g, SlabIndex &si, int64_t delta, const uint32_t *l
   const int n_slabs = (int)n;
   const int64_t W = (span + n_slabs - 1) / n_slabs;  // >= delta
   const int64_t N1 = N + 1;
+  if (!force && (int64_t)n_slabs * N1 > 2 * E) return TM_OK;  // cell tables would outweigh the entries
   // entries are addressed by int32 offsets: at most 2 E of them when W >= delta
   if (2 * E >= (int64_t)INT32_MAX || (int64_t)n_slabs * N1 >= (int64_t)INT32_MAX) return TM_OK;
   si.n_slabs = n_slabs;
@@ -372,7 +387,7 @@ int build_slab_view(tm_graph *g, SlabIndex &si, int64_t delta, const uint32_t *l
       return rc;
     k_slab_fill<<<grid_for(E, kFillTile), kFillThreads, kFillSmem, s>>>(g->owner[d].as<int32_t>(), g->rnk[d].as<uint32_t>(),
                                                g->npk[d].as<int2>(), E, s0, s1, si.slab_of.as<uint16_t>(),
-                                               L, deltaT, si.np[d].as<int2>(), si.rnk[d].as<uint32_t>());
+                                               L, S + 1, deltaT, si.np[d].as<int2>(), si.rnk[d].as<uint32_t>());
     TM_LAUNCHED("k_slab_fill");
     view->ptr[d] = ptr - (int64_t)s0 * N1;  // rows of slabs s0..s1, addressed by slab * (N + 1)
     view->np[d] = si.np[d].as<int2>();

@@ -17,6 +17,17 @@ from oracle.oracle import OracleGraph, column
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["auto", "slabs"])
+def view_mode(request, monkeypatch):
+    """Every parity case twice: the library's own choice of graph view (the
+    global CSR on these small graphs) and the time-slab view forced
+    (TM_SLABS=1, tm_slab.cu: windows spanning slab boundaries, halos,
+    single-slab horizons)."""
+    if request.param == "slabs":
+        monkeypatch.setenv("TM_SLABS", "1")
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def tmb():
     import paper_2604_12241_b200 as tmb

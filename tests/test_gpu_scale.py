@@ -42,7 +42,17 @@ def hi_medium():
     return _graph("hi-medium")
 
 
-def test_hi_small_full_array_parity(tmb):
+@pytest.fixture
+def slabs(request, monkeypatch):
+    """TM_SLABS: "auto" = the library's choice (the global view on this
+    shape), "1" = force the time-slab view (tm_slab.cu)."""
+    if request.param != "auto":
+        monkeypatch.setenv("TM_SLABS", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("slabs", ["auto", "1"], indirect=True)
+def test_hi_small_full_array_parity(tmb, slabs):
     from oracle.oracle import OracleGraph, column
     g0 = _graph("hi-small")
     names = list(tmb.FULL_PATTERN_SET)
@@ -63,7 +73,8 @@ def _blocks(E, n, size, seed):
         yield lo, lo + size
 
 
-def test_hi_medium_sampled_blocks(tmb, hi_medium):
+@pytest.mark.parametrize("slabs", ["auto", "1"], indirect=True)
+def test_hi_medium_sampled_blocks(tmb, hi_medium, slabs):
     from oracle.oracle import OracleGraph, column
     g0 = hi_medium
     names = list(tmb.FULL_PATTERN_SET)
@@ -160,7 +171,8 @@ def test_mine_distributed_nccl_world1(tmb):
         dist.destroy_process_group()
 
 
-def test_prepared_rank_views_match_full_call(tmb):
+@pytest.mark.parametrize("slabs", ["1"], indirect=True)
+def test_prepared_rank_views_match_full_call(tmb, slabs):
     """tm_mine_prepare on one rank's contiguous, time-ordered trigger range
     builds only that range's time slabs; mining the rank's pieces against
     those views must equal one full call (HI-Small, 4 simulated ranks x 3
