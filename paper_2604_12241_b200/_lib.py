@@ -146,7 +146,8 @@ ABI_VERSION = 7
 COUNTER_NAMES = ["trig", "u_walk", "u_item", "v_walk", "v_item", "window", "bisect32", "scan_call",
                  "scan_load", "pair_call", "bisect64", "inner_call", "inner_walk", "chain1", "chain2",
                  "chain3", "chain4", "close_call", "close_walk", "dom_task", "chain_task", "first",
-                 "inner_skip", "pulls", "queue_full", "slot_full", "useful_over", "bloom_over"]
+                 "inner_skip", "pulls", "queue_full", "slot_full", "useful_over", "bloom_over",
+                 "chain_over"]
 
 
 class TempmineError(RuntimeError):

@@ -22,7 +22,8 @@ LIB = HERE / "libtempmine_b200.so"
 # work counters, so the parity suite drives every exactness-preserving
 # fallback path (tests/test_gpu_fallbacks.py); never loaded by the package
 TINY_LIB = HERE / "libtempmine_b200_tinycaps.so"
-TINY_DEFINES = ("TM_TASK_CAP=64", "TM_SPLIT_CAP=8", "TM_BCAP=3", "TM_BLOOM_LIST=8", "TM_COUNTERS=1")
+TINY_DEFINES = ("TM_TASK_CAP=64", "TM_SPLIT_CAP=8", "TM_BCAP=3", "TM_BLOOM_LIST=8", "TM_CHAIN_CAP=16",
+                "TM_COUNTERS=1")
 SOURCES = ["tm_api.cu", "tm_sort.cu", "tm_graph.cu", "tm_slab.cu", "tm_mine.cu", "tm_members.cu", "tm_export.cu", "tm_instances.cu", "tm_vm.cu", "tm_ingest.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -17,7 +17,7 @@ enum CtrId {
   kCtrTrig, kCtrUWalk, kCtrUItem, kCtrVWalk, kCtrVItem, kCtrWin, kCtrBisect32, kCtrScanCall,
   kCtrScanLoad, kCtrPairCall, kCtrBisect64, kCtrInnerCall, kCtrInnerWalk, kCtrChain1, kCtrChain2,
   kCtrChain3, kCtrChain4, kCtrCloseCall, kCtrCloseWalk, kCtrDomTask, kCtrChainTask, kCtrFirst,
-  kCtrInnerSkip, kCtrPull, kCtrQueueFull, kCtrSlotFull, kCtrUsefulOver, kCtrBloomOver, kCtrN
+  kCtrInnerSkip, kCtrPull, kCtrQueueFull, kCtrSlotFull, kCtrUsefulOver, kCtrBloomOver, kCtrChainOver, kCtrN
 };
 #if TM_COUNTERS
 static __device__ unsigned long long tm_ctr[kCtrN];

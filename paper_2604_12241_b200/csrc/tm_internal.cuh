@@ -100,6 +100,9 @@ struct DevGroup {
   const uint16_t *slab_of;
   int64_t stride;
   const uint32_t *lo_tab;  // rank -> first rank with time >= uniq_time[rank] - delta
+  // per trigger row of the call (or null): (window start rank, slab) — read
+  // with the trigger's own edge fields instead of two lookups behind e_rank
+  const int2 *lo_slab;
   // own windows by edge id (or null): own[1][e] = window of e's source
   // out-run at e's time (u-out), own[0][e] = of e's destination in-run (v-in)
   const int2 *own[2];
@@ -254,7 +257,7 @@ struct tm_graph {
   tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2], peid[2], npk[2], owner[2];
 
   // mining scratch (grow-only)
-  tmb::DevBuf lo_tabs, own_tabs, bloom_lists, heavy_q, heavy_n, out_scratch, tasks, split_scratch;
+  tmb::DevBuf lo_tabs, own_tabs, bloom_lists, heavy_q, heavy_n, out_scratch, tasks, split_scratch, lo_slab, chain_q;
   tmb::DevBuf csv_buf;  // formatted feature CSV (tm_csv_format)
   int64_t csv_bytes = 0;
   tmb::DevBuf inst_buf;  // instance records (tm_collect_instances, tm_vm_collect)

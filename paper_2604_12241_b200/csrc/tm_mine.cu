@@ -91,12 +91,42 @@ struct Task {
 // TaskBloom): the chain walk skips nodes that cannot reach u in time
 struct TaskBloom;
 
+// A depth-1 chain node a1 = m of a trigger whose descent (chains a2.. of
+// cycle_5+) the trigger kernel defers: the deep, rare enumeration (0.08
+// depth-2 nodes per trigger at HI-Large) would otherwise keep its registers
+// allocated in the hot kernel.  k_mine_chains runs the records, one thread
+// each.
+struct ChainRec {
+  int32_t row, a1, wa, wb, grp;  // trigger row, a1, a1's out-window entries
+};
+struct ChainQ {
+  ChainRec *rec;
+  unsigned long long *count;
+  unsigned long long cap;
+  unsigned int *overflow;  // set when a deferred descent found no room (the call is re-run inline)
+};
+
 struct Queue {
   Task *q;
   unsigned long long *count;  // 64-bit: reservations past a full queue cannot wrap it
   int32_t cap;
   const TaskBloom *bloom;  // null: no filtering (warp kernel, small windows)
+  ChainQ chains;           // trigger kernel: deferred chain descents (rec null: none)
 };
+
+// warp-aggregated reservation of one record per calling lane
+__device__ __forceinline__ bool push_chain(const ChainQ &cq, int row, int grp, int a1, int wa, int wb) {
+  if (!cq.rec) return false;
+  const unsigned m = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(cq.count, (unsigned long long)__popc(m));
+  base = __shfl_sync(m, base, leader);
+  const unsigned long long k = base + (unsigned long long)__popc(m & ((1u << lane) - 1));
+  if (k >= cq.cap) return false;
+  cq.rec[k] = ChainRec{row, a1, wa, wb, grp};
+  return true;
+}
 
 // Bloom filters of the backward layers B_2..B_5 (B_1 = N-(u) \ {u, v},
 // B_{k+1} = N-(B_k) \ {u, v}, windowed): a node at depth j that closes at
@@ -462,13 +492,25 @@ __device__ __forceinline__ void cycles_a1(const Ctx &c, const CycGroup &cg, int 
   chain_level<1, PI>(c, cg, row, grp, path, ja, jb, cand, acc, qu);
 }
 
-template <bool PI>
+// DEFER (trigger kernel only): the descent below a1 is not enumerated here —
+// a narrow a1 becomes a chain record (k_mine_chains), a wide one a pull
+// task.  If a queue is full the record is dropped and the call's overflow
+// word set: tm_mine then runs the call again with DEFER off (the inline
+// enumeration), so no count is ever lost.
+template <bool PI, bool DEFER = false>
 __device__ __forceinline__ void cycles_from_a1(const Ctx &c, const CycGroup &cg, int row, int grp,
                                                int m, CycAcc &acc, const Queue &qu) {
   int path[kMaxChain] = {m, -1, -1, -1, -1};
   const Win w = window(c, 1, m);
   if (cg.mask & 2) close_at(cg, 1, close_count<0>(c, m, w, path), acc);
-  if (cg.maxd >= 2) cycles_a1<PI>(c, cg, row, grp, path, w, acc, qu);
+  if (cg.maxd < 2 || w.len() == 0) return;
+  if constexpr (DEFER) {
+    if (!(w.len() <= cg.deep_split ? push_chain(qu.chains, row, grp, m, w.a, w.b)
+                                   : emit_whole(qu, row, grp, 1 | kPullFlag, path, w.a, w.b)))
+      TM_CNT(kCtrChainOver, 1), atomicOr(qu.chains.overflow, 1u);
+  } else {
+    cycles_a1<PI>(c, cg, row, grp, path, w, acc, qu);
+  }
 }
 
 // a chain task resumes at level L with a1..a_L given (entries [ja, jb) of
@@ -515,7 +557,7 @@ __device__ __forceinline__ void u_item_sl(const Ctx &c, const DevPlans &P, const
 }
 
 // V item m (a distinct node of N+(v) \ {u, v}); parts: kV* bits
-template <bool PI, class Sink>
+template <bool PI, class Sink, bool DEFER = false>
 __device__ __forceinline__ void v_node(const Ctx &c, const DevPlans &P, const DevGroup &gr, int grp,
                                        int row, int m, Sink &sk, const Queue &qu, int parts) {
   TM_CNT(kCtrVItem, 1);
@@ -528,7 +570,7 @@ __device__ __forceinline__ void v_node(const Ctx &c, const DevPlans &P, const De
     CycAcc acc;
 #pragma unroll
     for (int e = 0; e < kMaxCyc; ++e) acc.e[e] = 0;
-    cycles_from_a1<PI>(c, gr.cyc, row, grp, m, acc, qu);
+    cycles_from_a1<PI, DEFER>(c, gr.cyc, row, grp, m, acc, qu);
 #pragma unroll
     for (int e = 0; e < kMaxCyc; ++e)
       if (e < gr.cyc.n && acc.e[e]) sk.col(gr.cyc.col[e], acc.e[e]);
@@ -623,11 +665,16 @@ __device__ __forceinline__ void flat_for(WarpShared &ws, int lane, int len, F &&
 #ifndef TM_WARP_MINB  // min resident blocks per SM for k_mine_warp (register cap)
 #define TM_WARP_MINB 16  // 64 registers at 64 threads: measured best
 #endif
-__global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
+#ifndef TM_WARP_MINB_DEFER  // the same with deferred chain descents (48 registers, no spills)
+#define TM_WARP_MINB_DEFER 20
+#endif
+template <bool DEFER>
+__global__ void __launch_bounds__(kThreads, DEFER ? TM_WARP_MINB_DEFER : TM_WARP_MINB) k_mine_warp(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     int64_t n_rows, long long *__restrict__ out, Queue qu, int32_t *__restrict__ split_rows,
     int32_t *__restrict__ split_n, int32_t *__restrict__ scratch, int32_t split_cap,
-    const int32_t *__restrict__ order) {
+    const int32_t *__restrict__ order, const unsigned int *__restrict__ gate) {
+  if (gate && *(volatile const unsigned int *)gate == 0) return;  // rescue pass not needed
   extern __shared__ long long stage_all[];  // [warp][32][S]: the staged (item) columns only —
                                             // shared memory left unused is L1 for the walkers
   __shared__ WarpShared wsh[kWarps];
@@ -656,12 +703,24 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
 
   for (int gi = 0; gi < P.ngroups; ++gi) {
     const DevGroup &gr = P.gr[gi];
-    const int slab = valid ? slab_of(gr, r) : 0;
-    Ctx c{gr.view, u, v, valid ? __ldg(gr.lo_tab + r) : 1u, r, {}, {}, {}, {}, (int64_t)slab * gr.stride};
+    int slab = 0;
+    uint32_t wlo = 1u;
+    if (valid) {
+      if (gr.lo_slab) {
+        const int2 ls = __ldg(gr.lo_slab + row);
+        wlo = (uint32_t)ls.x;
+        slab = ls.y;
+      } else {
+        slab = slab_of(gr, r);
+        wlo = __ldg(gr.lo_tab + r);
+      }
+    }
+    Ctx c{gr.view, u, v, wlo, r, {}, {}, {}, {}, (int64_t)slab * gr.stride};
+    // self-loop flags issued before the window searches they do not depend on
+    const int loop_u = valid ? (int)__ldg(g.loop + u) : 0, loop_v = valid ? (int)__ldg(g.loop + v) : 0;
     if (valid) trigger_windows(c, gr, (int)row);
     // per-lane columns: fan / degree (kernels.py:290-303), cycle_2 (:320-322)
     if (valid) {
-      const int loop_u = __ldg(g.loop + u), loop_v = __ldg(g.loop + v);  // once, not per column
       for (int i = 0; i < gr.ncols; ++i) {
         const int ci = gr.cols[i];
         const DevPlan &p = P.p[ci];
@@ -732,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, TM_WARP_MINB) k_mine_warp(
       const int m = sl.x;
       TM_CNT(kCtrVWalk, 1);
       if (m == co.u || m == co.v || !first_of(co, sl)) return;
-      v_node<false>(co, P, gr, gi, ws.rowid[o], m, sk, qu, ws.c3[o] >> kPartsShift);
+      v_node<false, SmemSink, DEFER>(co, P, gr, gi, ws.rowid[o], m, sk, qu, ws.c3[o] >> kPartsShift);
     });
     // whole-count columns: stack a * c (kernels.py:379-402), cycle_3 threshold
     if (valid) {
@@ -936,7 +995,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q,
-    int32_t *__restrict__ bloom_lists) {
+    int32_t *__restrict__ bloom_lists, const unsigned int *__restrict__ gate) {
+  if (gate && *(volatile const unsigned int *)gate == 0) return;
   const int n = (int)min(*in.count, (unsigned long long)in.cap);
   const int warps = gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -1086,11 +1146,52 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
   }
 }
 
+// deferred chain descents (push_chain), one record per thread: the trigger's
+// context is rebuilt (u's in-window closes every chain), chains a2.. below
+// a1 are enumerated with the task-kernel semantics (wide nodes: pull
+// candidates or chain tasks for the rounds that follow), counts are added
+// to the trigger's row
+__global__ void __launch_bounds__(256) k_mine_chains(const __grid_constant__ DevGraph g,
+                                                     const __grid_constant__ DevPlans P, int64_t lo,
+                                                     long long *__restrict__ out, ChainQ cq, Queue qu) {
+  const unsigned long long n = min(*cq.count, cq.cap);
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const ChainRec rc = cq.rec[i];
+    const DevGroup &gr = P.gr[rc.grp];
+    const int e = (int)(lo + rc.row);
+    const uint32_t r = __ldg(g.e_rank + e);
+    uint32_t wlo;
+    int slab;
+    if (gr.lo_slab) {
+      const int2 ls = __ldg(gr.lo_slab + rc.row);
+      wlo = (uint32_t)ls.x;
+      slab = ls.y;
+    } else {
+      wlo = __ldg(gr.lo_tab + r);
+      slab = slab_of(gr, r);
+    }
+    Ctx c{gr.view, __ldg(g.e_src + e), __ldg(g.e_dst + e), wlo, r, {}, {}, {}, {}, (int64_t)slab * gr.stride};
+    c.wui = window(c, 0, c.u);
+    CycAcc acc;
+#pragma unroll
+    for (int k = 0; k < kMaxCyc; ++k) acc.e[k] = 0;
+    int path[kMaxChain] = {rc.a1, -1, -1, -1, -1};
+    chain_level<1, true>(c, gr.cyc, rc.row, rc.grp, path, rc.wa, rc.wb, nullptr, acc, qu);
+    long long *orow = out + (int64_t)rc.row * P.n;
+#pragma unroll
+    for (int k = 0; k < kMaxCyc; ++k)
+      if (k < gr.cyc.n && acc.e[k])
+        atomicAdd(reinterpret_cast<unsigned long long *>(orow + gr.cyc.col[k]), (unsigned long long)acc.e[k]);
+  }
+}
+
 // rows whose slices went to domain tasks: whole-count columns from scratch
 __global__ void k_mine_finalize(const __grid_constant__ DevPlans P, long long *__restrict__ out,
                                 const int32_t *__restrict__ split_rows,
                                 const int32_t *__restrict__ split_n, const int32_t *__restrict__ scratch,
-                                int32_t split_cap) {
+                                int32_t split_cap, const unsigned int *__restrict__ gate) {
+  if (gate && *(volatile const unsigned int *)gate == 0) return;
   const int n = min(*split_n, split_cap);
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
     const int row = split_rows[2 * s], gi = split_rows[2 * s + 1];
@@ -1106,6 +1207,17 @@ __global__ void k_mine_finalize(const __grid_constant__ DevPlans P, long long *_
         orow[ci] = c3 >= p.min_size ? c3 : 0;
     }
   }
+}
+
+// per trigger row: (lo_tab[rank], slab of rank) — one coalesced 8-byte read
+// in the trigger kernel instead of two loads that wait for e_rank
+__global__ void k_lo_slab(const uint32_t *__restrict__ e_rank, int64_t lo, int64_t rows,
+                          const uint32_t *__restrict__ lo_tab, const uint16_t *__restrict__ slab_of,
+                          int2 *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const uint32_t r = __ldg(e_rank + lo + i);
+  out[i] = make_int2((int)__ldg(lo_tab + r), slab_of ? (int)__ldg(slab_of + r) : 0);
 }
 
 // lo_tab[r] = lower_bound(uniq_time, uniq_time[r] - delta)
@@ -1172,6 +1284,19 @@ __global__ void k_own_windows_slab(const __grid_constant__ DevGraph g, const uin
 
 using namespace tmb;
 
+#ifndef TM_LOSLAB
+#define TM_LOSLAB 1
+#endif
+
+// TM_DEFER=0: the trigger kernel enumerates chain descents inline (A/B)
+static bool defer_chains_enabled() {
+  static bool on = [] {
+    const char *e = getenv("TM_DEFER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // TM_ORDER=1 processes full-range calls in out-CSR (source) order; measured
 // neutral (HI-Small -3%, HI-Medium +2%), so edge-id order stays the default
 static bool source_order() {
@@ -1200,8 +1325,16 @@ static bool own_in_slabs() {
   return on;
 }
 
+static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
+                     int64_t *out, int out_on_device, void *stream, bool allow_defer);
+
 extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
                        int64_t *out, int out_on_device, void *stream) {
+  return mine_impl(g, plans, n_plans, lo, hi, out, out_on_device, stream, true);
+}
+
+static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_t lo, int64_t hi,
+                     int64_t *out, int out_on_device, void *stream, bool allow_defer) {
   if (!g) return fail(TM_E_BAD_ARG, "graph is NULL");
   if (n_plans < 0 || n_plans > kMaxPlans)
     return fail(TM_E_BAD_ARG, "n_plans must be in [0, " + std::to_string(kMaxPlans) + "]");
@@ -1286,6 +1419,9 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   if (own_on)
     for (int k = 0; k < dp.ngroups; ++k) n_own += ((dp.gr[k].need >> 1) & 1) + ((dp.gr[k].need >> 2) & 1);
   if (n_own && (rc = g->own_tabs.ensure_pooled(sizeof(int2) * (size_t)rows * n_own, s, g->stream))) return rc;
+#if TM_LOSLAB
+  if ((rc = g->lo_slab.ensure_pooled(sizeof(int2) * (size_t)rows * dp.ngroups, s, g->stream))) return rc;
+#endif
   const DevGraph dg = g->dev();
   int rounds = 0;
   int own_i = 0;
@@ -1339,6 +1475,15 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
       }
       dp.gr[k].own[dir] = tab;
     }
+#if TM_LOSLAB
+    {
+      int2 *ls = g->lo_slab.as<int2>() + (size_t)rows * k;
+      k_lo_slab<<<grid_for(rows, 256), 256, 0, s>>>(g->e_rank.as<uint32_t>(), lo, rows, dp.gr[k].lo_tab,
+                                                     dp.gr[k].slab_of, ls);
+      TM_LAUNCHED("k_lo_slab");
+      dp.gr[k].lo_slab = ls;
+    }
+#endif
     // Hand-off width for chain nodes: with short windows (mean windowed
     // degree <= 2) backward pruning in the task kernel wins for any node
     // wider than kDeepSplit; with long windows nearly every node is that
@@ -1370,7 +1515,7 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
 #else
   const int64_t split_cap = std::min<int64_t>(std::max<int64_t>(1 << 16, rows / 16), 1 << 22);
 #endif
-  if ((rc = g->heavy_n.ensure_pooled(sizeof(unsigned long long) * 4, s, g->stream)) ||
+  if ((rc = g->heavy_n.ensure_pooled(sizeof(unsigned long long) * 6, s, g->stream)) ||
       (rc = g->heavy_q.ensure_pooled(sizeof(int32_t) * 2 * (size_t)split_cap, s, g->stream)) ||
       (rc = g->split_scratch.ensure_pooled(sizeof(int32_t) * 3 * (size_t)split_cap, s, g->stream)) ||
       (rc = g->tasks.ensure_pooled(sizeof(Task) * (size_t)task_cap * 2, s, g->stream)))
@@ -1378,9 +1523,24 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   // [0] split rows (int32 in the low word), [1] [2] task queues A / B
   unsigned long long *cnt64 = g->heavy_n.as<unsigned long long>();
   int32_t *cnt = reinterpret_cast<int32_t *>(cnt64);
-  TM_CUDA(cudaMemsetAsync(cnt64, 0, sizeof(unsigned long long) * 4, s));
-  Queue qa{g->tasks.as<Task>(), cnt64 + 1, (int32_t)task_cap, nullptr};
-  Queue qb{g->tasks.as<Task>() + task_cap, cnt64 + 2, (int32_t)task_cap, nullptr};
+  // [4] (low word): overflow of the deferred chain descents, for the whole call
+  unsigned int *overflow = reinterpret_cast<unsigned int *>(cnt64 + 4);
+  TM_CUDA(cudaMemsetAsync(cnt64, 0, sizeof(unsigned long long) * 6, s));
+  Queue qa{g->tasks.as<Task>(), cnt64 + 1, (int32_t)task_cap, nullptr, ChainQ{}};
+  Queue qb{g->tasks.as<Task>() + task_cap, cnt64 + 2, (int32_t)task_cap, nullptr, ChainQ{}};
+  // [3] deferred chain descents of the trigger kernel (k_mine_chains)
+  bool any_chains = false;
+  for (int k = 0; k < dp.ngroups; ++k) any_chains |= dp.gr[k].cyc.maxd >= 2;
+  ChainQ cq{};
+  if (any_chains && allow_defer && defer_chains_enabled()) {
+#ifdef TM_CHAIN_CAP  // tiny-cap test builds: the overflow -> inline rescue path
+    const int64_t chain_cap = TM_CHAIN_CAP;
+#else
+    const int64_t chain_cap = std::max<int64_t>(1 << 20, rows / 2);
+#endif
+    if ((rc = g->chain_q.ensure_pooled(sizeof(ChainRec) * (size_t)chain_cap, s, g->stream))) return rc;
+    cq = ChainQ{g->chain_q.as<ChainRec>(), cnt64 + 3, (unsigned long long)chain_cap, overflow};
+  }
 
   for (int i = 0; i < n_plans; ++i) {
     const int f = plans[i].family;
@@ -1390,12 +1550,14 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   }
   const size_t smem = sizeof(long long) * kThreads * std::max(dp.n_stage, 1);
   if (smem > 48 * 1024)
-    TM_CUDA(cudaFuncSetAttribute(k_mine_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (const void *kf : {(const void *)k_mine_warp<true>, (const void *)k_mine_warp<false>})
+      TM_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // TM_CARVEOUT=pct: preferred shared-memory share of the L1/shared array
   // for the mining kernels (A/B: the walkers' loads are L1-cached)
   if (const char *co = getenv("TM_CARVEOUT")) {
     const int pct = atoi(co);
-    TM_CUDA(cudaFuncSetAttribute(k_mine_warp, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    TM_CUDA(cudaFuncSetAttribute(k_mine_warp<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    TM_CUDA(cudaFuncSetAttribute(k_mine_warp<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     TM_CUDA(cudaFuncSetAttribute(k_mine_tasks, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   }
   // Host output: mine the range in pieces and copy each finished piece back
@@ -1424,16 +1586,21 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
   g->prof_pending = g->prof;
   if (g->prof) TM_CUDA(cudaEventRecord(g->ev[0], s));
   const int64_t per = (rows + pieces - 1) / pieces;
-  for (int pc = 0; pc < pieces; ++pc) {
+  // one pass over piece pc: the trigger kernel (deferring chain descents when
+  // cq is set), the deferred descents, the task rounds, the split-row
+  // finalize.  gate != null: a rescue pass that runs only if the deferred
+  // pass overflowed (*gate != 0), recomputing every row inline.
+  auto run_piece = [&](int pc, bool defer, const unsigned int *gate) -> int {
     const int64_t r0 = std::min<int64_t>(rows, pc * per), r1 = std::min<int64_t>(rows, r0 + per);
     long long *po = d_out + r0 * n_plans;
     Queue a = qa, b = qb;
     DevPlans dpp = dp;  // own-window tables are indexed relative to the piece
-    for (int k = 0; k < dpp.ngroups; ++k)
+    for (int k = 0; k < dpp.ngroups; ++k) {
       for (int d = 0; d < 2; ++d)
         if (dpp.gr[k].own[d]) dpp.gr[k].own[d] += r0;
+      if (dpp.gr[k].lo_slab) dpp.gr[k].lo_slab += r0;
+    }
     TM_CUDA(cudaMemsetAsync(cnt64, 0, sizeof(unsigned long long) * 4, s));
-    // full-range device-output calls process triggers in out-CSR order
     // full-range device-output calls: triggers in time order when the edge
     // ids are not (slab views are then read slab by slab), or out-CSR order
     // (TM_ORDER=1 A/B); rows are always written by edge id
@@ -1444,30 +1611,49 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
                            : source_order() ? g->eid[1].as<int32_t>()
                            : (any_slabs && !g->ids_time_ordered) ? g->time_order.as<int32_t>()
                                                                  : nullptr;
-    k_mine_warp<<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
-        dg, dpp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt,
-        g->split_scratch.as<int32_t>(), (int32_t)split_cap, order);
-    TM_LAUNCHED("k_mine_warp");
-    if (g->prof && pc == pieces - 1) TM_CUDA(cudaEventRecord(g->ev[1], s));
+    if (defer) {
+      Queue aw = a;
+      aw.chains = cq;
+      k_mine_warp<true><<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
+          dg, dpp, lo + r0, r1 - r0, po, aw, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
+          (int32_t)split_cap, order, nullptr);
+      TM_LAUNCHED("k_mine_warp");
+      k_mine_chains<<<148 * 8, 256, 0, s>>>(dg, dpp, lo + r0, po, cq, a);
+      TM_LAUNCHED("k_mine_chains");
+    } else {
+      k_mine_warp<false><<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
+          dg, dpp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
+          (int32_t)split_cap, order, gate);
+      TM_LAUNCHED("k_mine_warp");
+    }
+    if (g->prof && pc == pieces - 1 && !gate) TM_CUDA(cudaEventRecord(g->ev[1], s));
     for (int r = 0; r < rounds; ++r) {
       TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(unsigned long long), s));
-      k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po,
-                                                      g->split_scratch.as<int32_t>(), a, b,
-                                                      g->bloom_lists.as<int32_t>());
+      k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
+                                                      b, g->bloom_lists.as<int32_t>(), gate);
       TM_LAUNCHED("k_mine_tasks");
       std::swap(a, b);
     }
     if (rounds > 0) {
-      k_mine_finalize<<<148, 256, 0, s>>>(dp, po, g->heavy_q.as<int32_t>(), cnt,
-                                          g->split_scratch.as<int32_t>(), (int32_t)split_cap);
+      k_mine_finalize<<<148, 256, 0, s>>>(dp, po, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
+                                          (int32_t)split_cap, gate);
       TM_LAUNCHED("k_mine_finalize");
     }
-    TM_CUDA(cudaMemcpyAsync(piece_split + pc, cnt, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (!gate) TM_CUDA(cudaMemcpyAsync(piece_split + pc, cnt, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    return TM_OK;
+  };
+  for (int pc = 0; pc < pieces; ++pc) {
+    const int64_t r0 = std::min<int64_t>(rows, pc * per), r1 = std::min<int64_t>(rows, r0 + per);
+    if ((rc = run_piece(pc, cq.rec != nullptr, nullptr))) return rc;
+    // device output: a deferred pass that overflowed is redone inline on the
+    // device (gated on the overflow word, no host round trip)
+    if (cq.rec && out_on_device && (rc = run_piece(pc, false, overflow))) return rc;
     if (pieces > 1) {
       TM_CUDA(cudaEventRecord(g->piece_ev[pc], s));
       TM_CUDA(cudaStreamWaitEvent(g->copy_stream, g->piece_ev[pc], 0));
-      TM_CUDA(cudaMemcpyAsync(out + r0 * n_plans, po, sizeof(long long) * (size_t)(r1 - r0) * n_plans,
-                              cudaMemcpyDeviceToHost, g->copy_stream));
+      TM_CUDA(cudaMemcpyAsync(out + r0 * n_plans, d_out + r0 * n_plans,
+                              sizeof(long long) * (size_t)(r1 - r0) * n_plans, cudaMemcpyDeviceToHost,
+                              g->copy_stream));
     }
   }
   if (g->prof) TM_CUDA(cudaEventRecord(g->ev[2], s));
@@ -1477,8 +1663,14 @@ extern "C" int tm_mine(tm_graph *g, const tm_plan_desc *plans, int n_plans, int6
                               cudaMemcpyDeviceToHost, s));
     int32_t ns[kHostPieces] = {};
     TM_CUDA(cudaMemcpyAsync(ns, piece_split, sizeof(int32_t) * pieces, cudaMemcpyDeviceToHost, s));
+    unsigned int ov = 0;
+    if (cq.rec) TM_CUDA(cudaMemcpyAsync(&ov, overflow, sizeof(ov), cudaMemcpyDeviceToHost, s));
     if (pieces > 1) TM_CUDA(cudaStreamSynchronize(g->copy_stream));
     TM_CUDA(cudaStreamSynchronize(s));
+    if (ov) {  // a deferred descent found no room: the whole call again, inline
+      TM_CUDA(g->end(s));
+      return mine_impl(g, plans, n_plans, lo, hi, out, out_on_device, stream, false);
+    }
     g->last.heavy_triggers = 0;
     for (int i = 0; i < pieces; ++i) g->last.heavy_triggers += ns[i];
   } else {

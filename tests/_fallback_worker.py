@@ -46,9 +46,18 @@ def main():
     for cfg, delta in cases:
         g0 = synth.generate(cfg)
         g = tmb.DeviceGraph(g0.src, g0.dst, g0.time)
-        got = tmb.mine_rows(g, [tmb.lower_plan(tmb.builtin_plan(n, delta)) for n in names], 0, g.edge_count)
+        descs = [tmb.lower_plan(tmb.builtin_plan(n, delta)) for n in names]
+        got = tmb.mine_rows(g, descs, 0, g.edge_count)  # host output: overflow -> whole call again
         want = OracleGraph(g0.src, g0.dst, g0.time).mine([column(n, delta) for n in names])
         bad += [f"{n}@{delta}" for j, n in enumerate(names) if not np.array_equal(got[:, j], want[:, j])]
+        # device output: overflow -> gated inline rescue pass on the device
+        import torch
+        dev = torch.empty((g.edge_count, len(descs)), dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        tmb.mine_rows_device(g, descs, 0, g.edge_count, dev.data_ptr())
+        torch.cuda.synchronize()
+        got_d = dev.cpu().numpy()
+        bad += [f"{n}@{delta}/device" for j, n in enumerate(names) if not np.array_equal(got_d[:, j], want[:, j])]
         g.free()
     print(json.dumps({"bad": bad, "counters": counters(lib)}))
 

@@ -39,5 +39,5 @@ def test_tiny_caps_variant_is_exact_and_hits_every_fallback():
     out = json.loads(res.stdout.strip().splitlines()[-1])
     assert out["bad"] == [], out
     c = out["counters"]
-    for k in ("queue_full", "slot_full", "useful_over", "bloom_over"):
+    for k in ("queue_full", "slot_full", "useful_over", "bloom_over", "chain_over"):
         assert c[k] > 0, (k, c)
