@@ -257,7 +257,7 @@ struct tm_graph {
   tmb::DevBuf ptr[2], nbr[2], rnk[2], eid[2], pkey[2], prev[2], peid[2], npk[2], owner[2];
 
   // mining scratch (grow-only)
-  tmb::DevBuf lo_tabs, own_tabs, bloom_lists, heavy_q, heavy_n, out_scratch, tasks, split_scratch, lo_slab, chain_q;
+  tmb::DevBuf lo_tabs, own_tabs, bloom_lists, heavy_q, heavy_n, out_scratch, tasks, split_scratch, lo_slab, chain_q, split_win;
   tmb::DevBuf csv_buf;  // formatted feature CSV (tm_csv_format)
   int64_t csv_bytes = 0;
   tmb::DevBuf inst_buf;  // instance records (tm_collect_instances, tm_vm_collect)

@@ -98,6 +98,7 @@ struct TaskBloom;
 // each.
 struct ChainRec {
   int32_t row, a1, wa, wb, grp;  // trigger row, a1, a1's out-window entries
+  int32_t ua, ub;                // the trigger's u-in window (every close reads it)
 };
 struct ChainQ {
   ChainRec *rec;
@@ -115,7 +116,8 @@ struct Queue {
 };
 
 // warp-aggregated reservation of one record per calling lane
-__device__ __forceinline__ bool push_chain(const ChainQ &cq, int row, int grp, int a1, int wa, int wb) {
+__device__ __forceinline__ bool push_chain(const ChainQ &cq, int row, int grp, int a1, int wa, int wb,
+                                           const Win &ui) {
   if (!cq.rec) return false;
   const unsigned m = __activemask();
   const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
@@ -124,7 +126,7 @@ __device__ __forceinline__ bool push_chain(const ChainQ &cq, int row, int grp, i
   base = __shfl_sync(m, base, leader);
   const unsigned long long k = base + (unsigned long long)__popc(m & ((1u << lane) - 1));
   if (k >= cq.cap) return false;
-  cq.rec[k] = ChainRec{row, a1, wa, wb, grp};
+  cq.rec[k] = ChainRec{row, a1, wa, wb, grp, ui.a, ui.b};
   return true;
 }
 
@@ -505,7 +507,7 @@ __device__ __forceinline__ void cycles_from_a1(const Ctx &c, const CycGroup &cg,
   if (cg.mask & 2) close_at(cg, 1, close_count<0>(c, m, w, path), acc);
   if (cg.maxd < 2 || w.len() == 0) return;
   if constexpr (DEFER) {
-    if (!(w.len() <= cg.deep_split ? push_chain(qu.chains, row, grp, m, w.a, w.b)
+    if (!(w.len() <= cg.deep_split ? push_chain(qu.chains, row, grp, m, w.a, w.b, c.wui)
                                    : emit_whole(qu, row, grp, 1 | kPullFlag, path, w.a, w.b)))
       TM_CNT(kCtrChainOver, 1), atomicOr(qu.chains.overflow, 1u);
   } else {
@@ -668,21 +670,19 @@ __device__ __forceinline__ void flat_for(WarpShared &ws, int lane, int len, F &&
 #ifndef TM_WARP_MINB_DEFER  // the same with deferred chain descents (48 registers, no spills)
 #define TM_WARP_MINB_DEFER 20
 #endif
+// one block's 64 triggers (virtual block vb of the call)
 template <bool DEFER>
-__global__ void __launch_bounds__(kThreads, DEFER ? TM_WARP_MINB_DEFER : TM_WARP_MINB) k_mine_warp(
-    const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
-    int64_t n_rows, long long *__restrict__ out, Queue qu, int32_t *__restrict__ split_rows,
-    int32_t *__restrict__ split_n, int32_t *__restrict__ scratch, int32_t split_cap,
-    const int32_t *__restrict__ order, const unsigned int *__restrict__ gate) {
-  if (gate && *(volatile const unsigned int *)gate == 0) return;  // rescue pass not needed
-  extern __shared__ long long stage_all[];  // [warp][32][S]: the staged (item) columns only —
-                                            // shared memory left unused is L1 for the walkers
-  __shared__ WarpShared wsh[kWarps];
+__device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P, int64_t lo, int64_t n_rows,
+                                           long long *__restrict__ out, const Queue &qu,
+                                           int32_t *__restrict__ split_rows, int32_t *__restrict__ split_n,
+                                           int32_t *__restrict__ scratch, int4 *__restrict__ split_win,
+                                           int32_t split_cap, const int32_t *__restrict__ order, int64_t vb,
+                                           long long *stage_all, WarpShared *wsh) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpShared &ws = wsh[warp];
   const int C = P.n, S = P.n_stage;
   long long *stage = stage_all + (size_t)warp * 32 * S;
-  const int64_t wrow0 = (int64_t)blockIdx.x * kThreads + warp * 32;
+  const int64_t wrow0 = vb * kThreads + warp * 32;
   const int64_t pos = wrow0 + lane;  // position in processing order
   const bool valid = pos < n_rows;
   // trigger order: edge-id order, or (full range only) `order` = the
@@ -755,6 +755,10 @@ __global__ void __launch_bounds__(kThreads, DEFER ? TM_WARP_MINB_DEFER : TM_WARP
         } else {
           split_rows[2 * slot] = (int)row;
           split_rows[2 * slot + 1] = gi;
+          // the trigger's windows, read back by its tasks (no re-search
+          // of hub runs per task)
+          split_win[2 * slot] = make_int4(c.wui.a, c.wui.b, c.wuo.a, c.wuo.b);
+          split_win[2 * slot + 1] = make_int4(c.wvi.a, c.wvi.b, c.wvo.a, c.wvo.b);
         }
       }
       if (slot != -2) {
@@ -831,6 +835,27 @@ __global__ void __launch_bounds__(kThreads, DEFER ? TM_WARP_MINB_DEFER : TM_WARP
     r0 += dq;
     k0 += dr;
     if (k0 >= S) k0 -= S, ++r0;
+  }
+}
+
+// The trigger kernel.  gate != null (the rescue pass): a small grid that
+// exits at once unless the deferred pass overflowed; virtual blocks are
+// strided over the grid, so the rescue needs no full-size launch.
+template <bool DEFER>
+__global__ void __launch_bounds__(kThreads, DEFER ? TM_WARP_MINB_DEFER : TM_WARP_MINB) k_mine_warp(
+    const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
+    int64_t n_rows, long long *__restrict__ out, Queue qu, int32_t *__restrict__ split_rows,
+    int32_t *__restrict__ split_n, int32_t *__restrict__ scratch, int4 *__restrict__ split_win,
+    int32_t split_cap, const int32_t *__restrict__ order, const unsigned int *__restrict__ gate) {
+  if (gate && *(volatile const unsigned int *)gate == 0) return;  // rescue pass not needed
+  extern __shared__ long long stage_all[];  // [warp][32][S]: the staged (item) columns only —
+                                            // shared memory left unused is L1 for the walkers
+  __shared__ WarpShared wsh[kWarps];
+  const int64_t nvb = (n_rows + kThreads - 1) / kThreads;
+  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    mine_block<DEFER>(g, P, lo, n_rows, out, qu, split_rows, split_n, scratch, split_win, split_cap, order, vb,
+                      stage_all, wsh);
+    __syncthreads();  // the next virtual block re-uses the shared state
   }
 }
 
@@ -995,7 +1020,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q,
-    int32_t *__restrict__ bloom_lists, const unsigned int *__restrict__ gate) {
+    int32_t *__restrict__ bloom_lists, const int4 *__restrict__ split_win,
+    const unsigned int *__restrict__ gate) {
   if (gate && *(volatile const unsigned int *)gate == 0) return;
   const int n = (int)min(*in.count, (unsigned long long)in.cap);
   const int warps = gridDim.x * (blockDim.x >> 5);
@@ -1021,7 +1047,18 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const uint32_t r = __ldg(g.e_rank + e);
     Ctx c{gr.view, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {},
           (int64_t)slab_of(gr, r) * gr.stride};
-    trigger_windows(c, gr, t.row);
+    const bool item_task = t.level == kLvlDomU || t.level == kLvlDomV || t.level == kLvlPullV;
+    if (item_task && t.path[0] >= 0) {  // a split row: the trigger kernel stored its windows
+      const int4 w0 = __ldg(split_win + 2 * t.path[0]), w1 = __ldg(split_win + 2 * t.path[0] + 1);
+      c.wui = Win{w0.x, w0.y};
+      c.wuo = Win{w0.z, w0.w};
+      c.wvi = Win{w1.x, w1.y};
+      c.wvo = Win{w1.z, w1.w};
+    } else if (!item_task) {  // chain tasks close into u's in-window only
+      c.wui = window(c, 0, c.u);
+    } else {
+      trigger_windows(c, gr, t.row);
+    }
     // chain walks of this task get the trigger's backward-layer filters
     Queue next = next_q;
     const bool chains = t.level != kLvlDomU && !(t.level == kLvlDomV && !(t.pad0 & kVCyc));
@@ -1172,7 +1209,7 @@ __global__ void __launch_bounds__(256) k_mine_chains(const __grid_constant__ Dev
       slab = slab_of(gr, r);
     }
     Ctx c{gr.view, __ldg(g.e_src + e), __ldg(g.e_dst + e), wlo, r, {}, {}, {}, {}, (int64_t)slab * gr.stride};
-    c.wui = window(c, 0, c.u);
+    c.wui = Win{rc.ua, rc.ub};
     CycAcc acc;
 #pragma unroll
     for (int k = 0; k < kMaxCyc; ++k) acc.e[k] = 0;
@@ -1518,6 +1555,7 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
   if ((rc = g->heavy_n.ensure_pooled(sizeof(unsigned long long) * 6, s, g->stream)) ||
       (rc = g->heavy_q.ensure_pooled(sizeof(int32_t) * 2 * (size_t)split_cap, s, g->stream)) ||
       (rc = g->split_scratch.ensure_pooled(sizeof(int32_t) * 3 * (size_t)split_cap, s, g->stream)) ||
+      (rc = g->split_win.ensure_pooled(sizeof(int4) * 2 * (size_t)split_cap, s, g->stream)) ||
       (rc = g->tasks.ensure_pooled(sizeof(Task) * (size_t)task_cap * 2, s, g->stream)))
     return rc;
   // [0] split rows (int32 in the low word), [1] [2] task queues A / B
@@ -1616,21 +1654,25 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
       aw.chains = cq;
       k_mine_warp<true><<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
           dg, dpp, lo + r0, r1 - r0, po, aw, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
-          (int32_t)split_cap, order, nullptr);
+          g->split_win.as<int4>(), (int32_t)split_cap, order, nullptr);
       TM_LAUNCHED("k_mine_warp");
       k_mine_chains<<<148 * 8, 256, 0, s>>>(dg, dpp, lo + r0, po, cq, a);
       TM_LAUNCHED("k_mine_chains");
     } else {
-      k_mine_warp<false><<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
+      // the gated rescue pass: a resident-size grid strides over the rows
+      const unsigned grid = gate ? std::min<unsigned>(grid_for(r1 - r0, kThreads), 148 * 16)
+                                 : grid_for(r1 - r0, kThreads);
+      k_mine_warp<false><<<grid, kThreads, smem, s>>>(
           dg, dpp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
-          (int32_t)split_cap, order, gate);
+          g->split_win.as<int4>(), (int32_t)split_cap, order, gate);
       TM_LAUNCHED("k_mine_warp");
     }
     if (g->prof && pc == pieces - 1 && !gate) TM_CUDA(cudaEventRecord(g->ev[1], s));
     for (int r = 0; r < rounds; ++r) {
       TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(unsigned long long), s));
       k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
-                                                      b, g->bloom_lists.as<int32_t>(), gate);
+                                                      b, g->bloom_lists.as<int32_t>(), g->split_win.as<int4>(),
+                                                      gate);
       TM_LAUNCHED("k_mine_tasks");
       std::swap(a, b);
     }
