@@ -175,8 +175,14 @@ __global__ void __launch_bounds__(kTileThreads) k_slab_tile_ptrs(
 // every slab chunk leaves in coalesced stores (the direct per-slot scatter
 // wrote 12-byte pieces into ~100 slab regions per warp: 7.5 ms per direction
 // at HI-Large).
-constexpr int kFillThreads = 512;
-constexpr int kFillPer = 4;                           // global slots per thread
+#ifndef TM_FILL_THREADS
+#define TM_FILL_THREADS 1024  // measured: 1024 x 2 slots 80.7 ms, 512 x 4 81.7, 256 x 8 83.3, 1024 x 4 83.0 (HI-Large call)
+#endif
+#ifndef TM_FILL_PER
+#define TM_FILL_PER 2
+#endif
+constexpr int kFillThreads = TM_FILL_THREADS;
+constexpr int kFillPer = TM_FILL_PER;                 // global slots per thread
 constexpr int kFillTile = kFillThreads * kFillPer;   // 2048 global slots per block
 constexpr int kFillItems = 2 * kFillTile;    // at most two copies per slot
 constexpr int kMaxSlabBins = 128;            // kMaxSlabs
