@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, DEFER ? TM_WARP_MINB_DEFER : TM_WARP
   for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
     mine_block<DEFER>(g, P, lo, n_rows, out, qu, split_rows, split_n, scratch, split_win, split_cap, order, vb,
                       stage_all, wsh);
-    __syncthreads();  // the next virtual block re-uses the shared state
+    if (vb + gridDim.x < nvb) __syncthreads();  // the next virtual block re-uses the shared state
   }
 }
 

@@ -81,15 +81,13 @@ __global__ void k_slab_of(const uint32_t *__restrict__ S, int n_slabs, int64_t R
 // Cells are owner-major: cell (x, s) = x * ns + s.
 // Only slabs [s0, s1] are built (a prepared view covers the slabs of one
 // rank's trigger range); cell column of slab s = s - s0, ns = s1 - s0 + 1.
-__global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *__restrict__ rnk,
-                             const int32_t *__restrict__ ptr, int64_t E, int s0, int s1,
-                             const uint16_t *__restrict__ slab_of, const uint32_t *__restrict__ S,
-                             const uint32_t *__restrict__ L, int32_t *__restrict__ startT,
-                             int32_t *__restrict__ endT) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= E) return;
-  const uint32_t r = __ldg(rnk + j);
-  if (r < __ldg(L + s0) || r >= __ldg(S + s1 + 1)) return;  // in no built slab (no slab_of gather)
+// One thread per 4 consecutive global slots (one 16-byte rank load): a
+// prepared view of 1/N of the slabs skips most slots after that load.
+__device__ __forceinline__ void slab_edge_slot(int64_t j, uint32_t r, const int32_t *__restrict__ owner,
+                                               const uint32_t *__restrict__ rnk, const int32_t *__restrict__ ptr,
+                                               int s0, int s1, const uint16_t *__restrict__ slab_of,
+                                               const uint32_t *__restrict__ S, const uint32_t *__restrict__ L,
+                                               int32_t *__restrict__ startT, int32_t *__restrict__ endT) {
   int s = __ldg(slab_of + r);
   const int x = __ldg(owner + j);
   const int a = __ldg(ptr + x), b = __ldg(ptr + x + 1);
@@ -101,6 +99,28 @@ __global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *
     if (j == a || rp < __ldg(L + s)) st[s] = (int32_t)j;          // opens x's run in slab s
     if (j + 1 == b || rn >= __ldg(S + s + 1)) en[s] = (int32_t)(j + 1);  // closes it
   }
+}
+
+__global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *__restrict__ rnk,
+                             const int32_t *__restrict__ ptr, int64_t E, int s0, int s1,
+                             const uint16_t *__restrict__ slab_of, const uint32_t *__restrict__ S,
+                             const uint32_t *__restrict__ L, int32_t *__restrict__ startT,
+                             int32_t *__restrict__ endT) {
+  const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= E) return;
+  const uint32_t r_lo = __ldg(L + s0), r_hi = __ldg(S + s1 + 1);  // ranks held by slabs s0..s1
+  uint32_t r4[4];
+  if (j0 + 4 <= E) {  // rank arrays are 16-byte aligned (device buffers)
+    const uint4 q = __ldg(reinterpret_cast<const uint4 *>(rnk + j0));
+    r4[0] = q.x; r4[1] = q.y; r4[2] = q.z; r4[3] = q.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r4[k] = j0 + k < E ? __ldg(rnk + j0 + k) : 0xffffffffu;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (j0 + k < E && r4[k] >= r_lo && r4[k] < r_hi)
+      slab_edge_slot(j0 + k, r4[k], owner, rnk, ptr, s0, s1, slab_of, S, L, startT, endT);
 }
 
 // The slab-major offsets ptrS[s][x] = (entries of slabs < s) + (entries of
@@ -370,7 +390,7 @@ int build_slab_view(tm_graph *g, SlabIndex &si, int64_t delta, const uint32_t *l
     int32_t *startS = si.start[d].as<int32_t>(), *ptr = si.ptr[d].as<int32_t>();
     // cells of owners without entries in a slab stay 0 - 0 (empty runs)
     TM_CUDA(cudaMemsetAsync(startT, 0, sizeof(int32_t) * 2 * (size_t)cells, s));
-    k_slab_edges<<<grid_for(E, kB), kB, 0, s>>>(g->owner[d].as<int32_t>(), g->rnk[d].as<uint32_t>(),
+    k_slab_edges<<<grid_for((E + 3) / 4, kB), kB, 0, s>>>(g->owner[d].as<int32_t>(), g->rnk[d].as<uint32_t>(),
                                                 g->ptr[d].as<int32_t>(), E, s0, s1,
                                                 si.slab_of.as<uint16_t>(), S, L, startT, endT);
     TM_LAUNCHED("k_slab_edges");

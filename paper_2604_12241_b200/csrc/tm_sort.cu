@@ -48,12 +48,21 @@ __global__ void __launch_bounds__(kSortThreads) k_digit_hist(const uint64_t *__r
     counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
 }
 
+// Stable scatter, onesweep-style: every item's rank within its digit is
+// computed as before (warp match + shared per-warp counts), the tile is then
+// regrouped by digit in shared memory, and the digit runs leave in
+// consecutive addresses (the direct scatter wrote 12 bytes per item into up
+// to 256 regions per warp step).
 __global__ void __launch_bounds__(kSortThreads) k_digit_scatter(
     const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, int64_t ntiles,
     const uint32_t *__restrict__ offsets) {
   __shared__ uint32_t wcnt[kWarps][kRadix];
   __shared__ uint32_t goff[kRadix];
+  __shared__ uint32_t loff[kRadix];  // digit's first slot in the regrouped tile
+  extern __shared__ unsigned char scatter_smem[];
+  uint64_t *sk = reinterpret_cast<uint64_t *>(scatter_smem);  // [kTile]
+  uint32_t *sv = reinterpret_cast<uint32_t *>(sk + kTile);    // [kTile]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < kWarps * kRadix; i += kSortThreads) (&wcnt[0][0])[i] = 0;
   for (int d = threadIdx.x; d < kRadix; d += kSortThreads)
@@ -84,6 +93,8 @@ __global__ void __launch_bounds__(kSortThreads) k_digit_scatter(
     __syncwarp();
   }
   __syncthreads();
+  // per digit: exclusive prefix over warps (stable order) and the digit's
+  // total -> loff = exclusive prefix of the totals over digits
   for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
     uint32_t run = 0;
 #pragma unroll
@@ -92,16 +103,42 @@ __global__ void __launch_bounds__(kSortThreads) k_digit_scatter(
       wcnt[w][d] = run;
       run += c;
     }
+    loff[d] = run;  // total, scanned below
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the 256 digit totals by warp 0
+    uint32_t carry = 0;
+    for (int c0 = 0; c0 < kRadix; c0 += 32) {
+      const uint32_t x = loff[c0 + lane];
+      uint32_t inc = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      loff[c0 + lane] = carry + inc - x;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
   }
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
     if (pos[it] != 0xffffffffu) {
       unsigned d = (unsigned)(k[it] >> shift) & 0xffu;
-      uint32_t o = goff[d] + wcnt[warp][d] + pos[it];
-      kout[o] = k[it];
-      vout[o] = v[it];
+      const uint32_t q = loff[d] + wcnt[warp][d] + pos[it];
+      sk[q] = k[it];
+      sv[q] = v[it];
     }
+  }
+  __syncthreads();
+  const int64_t tile0 = (int64_t)blockIdx.x * kTile;
+  const int nt = (int)(n - tile0 < kTile ? n - tile0 : kTile);
+  for (int q = threadIdx.x; q < nt; q += kSortThreads) {
+    const uint64_t key = sk[q];
+    const unsigned d = (unsigned)(key >> shift) & 0xffu;
+    const uint32_t o = goff[d] + (q - loff[d]);
+    kout[o] = key;
+    vout[o] = sv[q];
   }
 }
 
@@ -193,6 +230,8 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *v
   const int64_t ntiles = (n + kTile - 1) / kTile;
   uint32_t *counts = nullptr;
   TM_CUDA(pool_malloc((void **)&counts, sizeof(uint32_t) * kRadix * ntiles, s));
+  constexpr int kScatterSmem = kTile * (sizeof(uint64_t) + sizeof(uint32_t));  // 48 KB
+  TM_CUDA(cudaFuncSetAttribute(k_digit_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem));
   uint64_t *ka = keys, *kb = ktmp;
   uint32_t *va = vals, *vb = vtmp;
   for (int shift = 0; shift < nbits; shift += 8) {
@@ -200,8 +239,8 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *v
     TM_LAUNCHED("k_digit_hist");
     int rc = exclusive_scan_u32(counts, counts, kRadix * ntiles, s);
     if (rc) return rc;
-    k_digit_scatter<<<(unsigned)ntiles, kSortThreads, 0, s>>>(ka, va, kb, vb, n, shift, ntiles,
-                                                              counts);
+    k_digit_scatter<<<(unsigned)ntiles, kSortThreads, kScatterSmem, s>>>(ka, va, kb, vb, n, shift, ntiles,
+                                                                         counts);
     TM_LAUNCHED("k_digit_scatter");
     uint64_t *kt = ka; ka = kb; kb = kt;
     uint32_t *vt = va; va = vb; vb = vt;

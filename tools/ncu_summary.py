@@ -117,7 +117,7 @@ def main():
     out.write_text("\n".join(md) + "\n")
     tj = ROOT / "profiles" / "ncu_traffic.json"
     cur = json.loads(tj.read_text()) if tj.exists() else {}
-    cur[a.config] = traffic
+    cur.setdefault(a.config, {})["kernels"] = traffic  # per-kernel; launch_list.py adds step_dram_bytes
     tj.write_text(json.dumps(cur, indent=1) + "\n")
     print(out.read_text())
 
