@@ -1567,14 +1567,22 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
   Queue qa{g->tasks.as<Task>(), cnt64 + 1, (int32_t)task_cap, nullptr, ChainQ{}};
   Queue qb{g->tasks.as<Task>() + task_cap, cnt64 + 2, (int32_t)task_cap, nullptr, ChainQ{}};
   // [3] deferred chain descents of the trigger kernel (k_mine_chains)
-  bool any_chains = false;
-  for (int k = 0; k < dp.ngroups; ++k) any_chains |= dp.gr[k].cyc.maxd >= 2;
+  // Deferral pays for short windows, where a1's window is a few entries and
+  // records are fewer than triggers; with long windows (mean windowed degree
+  // > 2, the deep_split switch above) nearly every V item would become a
+  // record and the queue would overflow into the rescue pass, so the
+  // trigger kernel enumerates inline there.
+  bool any_chains = false, long_windows = false;
+  for (int k = 0; k < dp.ngroups; ++k) {
+    any_chains |= dp.gr[k].cyc.maxd >= 2;
+    long_windows |= dp.gr[k].cyc.maxd >= 2 && dp.gr[k].cyc.deep_split != kDeepSplit;
+  }
   ChainQ cq{};
-  if (any_chains && allow_defer && defer_chains_enabled()) {
+  if (any_chains && !long_windows && allow_defer && defer_chains_enabled()) {
 #ifdef TM_CHAIN_CAP  // tiny-cap test builds: the overflow -> inline rescue path
     const int64_t chain_cap = TM_CHAIN_CAP;
 #else
-    const int64_t chain_cap = std::max<int64_t>(1 << 20, rows / 2);
+    const int64_t chain_cap = std::max<int64_t>(1 << 20, rows);
 #endif
     if ((rc = g->chain_q.ensure_pooled(sizeof(ChainRec) * (size_t)chain_cap, s, g->stream))) return rc;
     cq = ChainQ{g->chain_q.as<ChainRec>(), cnt64 + 3, (unsigned long long)chain_cap, overflow};

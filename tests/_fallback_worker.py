@@ -41,6 +41,10 @@ def main():
         # alpha = 2.1: one giant hub, many split rows
         (synth.SynthConfig(3000, 60000, 8 * 86400, seed=11, powerlaw_exponent=2.1,
                            plants=(synth.PlantSpec("sg_count", 40),)), 86400),
+        # short windows (mean windowed degree < 2): the trigger kernel defers
+        # chain descents and the tiny chain queue overflows into the rescue
+        (synth.SynthConfig(4000, 80000, 30 * 86400, seed=5, powerlaw_exponent=1.0,
+                           plants=(synth.PlantSpec("cycle_4", 40),)), 2 * 86400),
     ]
     bad = []
     for cfg, delta in cases:
