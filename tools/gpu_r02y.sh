@@ -1,0 +1,7 @@
+# rank fences A/B + tests
+set -x
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/r02y_gpu_tests.log 2>&1
+for cfg in hi-large hi-medium hi-small; do
+  timeout 900 python tools/ab_libs.py $cfg ablibs/fence256.so ablibs/nofence.so ablibs/fence64.so ablibs/fence1k.so >> gpurun_out/r02y_ab.jsonl 2>> gpurun_out/r02y_ab.err
+done
