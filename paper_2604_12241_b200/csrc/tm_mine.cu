@@ -1017,6 +1017,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 //                         nodes, or chain tasks for the next round
 //   level 1..4            a piece of a chain node's window
 // Each kind feeds ONE call site of the item / chain code below.
+// MODE 0: every task kind, chain descents inline (calls without deferral
+// and the rescue pass); MODE 1: the item kinds (domain U / V, pull-V) with
+// their chain descents deferred to records (no chain code in this kernel:
+// fewer registers, no Bloom build); MODE 2: the chain kinds only.
+template <int MODE>
 __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q,
@@ -1042,12 +1047,13 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
   for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
     const Task t = in.q[i];
     if (t.row < 0) continue;
+    const bool item_task = t.level == kLvlDomU || t.level == kLvlDomV || t.level == kLvlPullV;
+    if ((MODE == 1 && !item_task) || (MODE == 2 && item_task)) continue;
     const int e = (int)(lo + t.row);
     const DevGroup &gr = P.gr[t.grp];
     const uint32_t r = __ldg(g.e_rank + e);
     Ctx c{gr.view, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {},
           (int64_t)slab_of(gr, r) * gr.stride};
-    const bool item_task = t.level == kLvlDomU || t.level == kLvlDomV || t.level == kLvlPullV;
     if (item_task && t.path[0] >= 0) {  // a split row: the trigger kernel stored its windows
       const int4 w0 = __ldg(split_win + 2 * t.path[0]), w1 = __ldg(split_win + 2 * t.path[0] + 1);
       c.wui = Win{w0.x, w0.y};
@@ -1061,7 +1067,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     }
     // chain walks of this task get the trigger's backward-layer filters
     Queue next = next_q;
-    const bool chains = t.level != kLvlDomU && !(t.level == kLvlDomV && !(t.pad0 & kVCyc));
+    const bool chains = MODE != 1 && t.level != kLvlDomU && !(t.level == kLvlDomV && !(t.pad0 & kVCyc));
     // (narrow windows are cheaper to walk than the filters are to build)
     if (chains && gr.cyc.maxd >= 2 && c.u != c.v && c.wui.len() > 0 && t.b - t.a > kBloomMin) {
       // layers up to the one a depth-1 node needs for the deepest close
@@ -1070,6 +1076,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     }
     long long *orow = out + (int64_t)t.row * P.n;
     int use[kBCap];
+    if constexpr (MODE != 2) {
     if (t.level == kLvlDomU) {
       GlobalSink sk{orow, scratch + 3 * (t.path[0] >= 0 ? t.path[0] : 0)};
 #if TM_TMA_TASKS
@@ -1116,7 +1123,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
               for (int j = t.a + lane; j < t.b; j += 32) {
                 const int m = __ldg(c.g.np[1] + j).x;
                 if (m == c.u || m == c.v || !first_in_window(c, 1, j)) continue;
-                if (redo & kVGs) v_node<true>(c, P, gr, t.grp, t.row, m, sk, next, kVGs);
+                if (redo & kVGs) v_node<true, GlobalSink, MODE == 1>(c, P, gr, t.grp, t.row, m, sk, next, kVGs);
               }
             } else {
               parts = redo;
@@ -1149,9 +1156,12 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
           m = sl.x;
           if (m == c.u || m == c.v || !first_of(c, sl)) continue;
         }
-        v_node<true>(c, P, gr, t.grp, t.row, m, sk, next, parts);
+        v_node<true, GlobalSink, MODE == 1>(c, P, gr, t.grp, t.row, m, sk, next, parts);
       }
-    } else {  // a chain node's window (or its useful nodes)
+    }
+    }  // MODE != 2
+    if constexpr (MODE != 1) {
+    if (!item_task) {  // a chain node's window (or its useful nodes)
       CycAcc acc;
 #pragma unroll
       for (int k = 0; k < kMaxCyc; ++k) acc.e[k] = 0;
@@ -1180,6 +1190,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
           atomicAdd(reinterpret_cast<unsigned long long *>(orow + gr.cyc.col[k]), (unsigned long long)sum);
       }
     }
+    }  // MODE != 1
   }
 }
 
@@ -1324,6 +1335,15 @@ using namespace tmb;
 #ifndef TM_LOSLAB
 #define TM_LOSLAB 1
 #endif
+
+// TM_SPLIT_TASKS=1: item / chain task kernels with deferral at any size (tests)
+static bool split_tasks_forced() {
+  static bool on = [] {
+    const char *e = getenv("TM_SPLIT_TASKS");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 
 // TM_DEFER=0: the trigger kernel enumerates chain descents inline (A/B)
 static bool defer_chains_enabled() {
@@ -1604,7 +1624,8 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
     const int pct = atoi(co);
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    TM_CUDA(cudaFuncSetAttribute(k_mine_tasks, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    for (const void *kf : {(const void *)k_mine_tasks<0>, (const void *)k_mine_tasks<1>, (const void *)k_mine_tasks<2>})
+      TM_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   }
   // Host output: mine the range in pieces and copy each finished piece back
   // on a copy stream while the next piece is mined — the D2H of the int64
@@ -1676,12 +1697,34 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
       TM_LAUNCHED("k_mine_warp");
     }
     if (g->prof && pc == pieces - 1 && !gate) TM_CUDA(cudaEventRecord(g->ev[1], s));
+    // big calls: item tasks defer too (a spill-free item-task kernel; HI-Large
+    // task rounds 9.6 -> 8.4 ms); small ones keep one launch per round (the
+    // two extra launches per round cost more there: HI-Small 0.85 -> 0.99 ms)
+    const bool split_tasks = defer && (r1 - r0 >= (int64_t)1 << 24 || split_tasks_forced());
     for (int r = 0; r < rounds; ++r) {
       TM_CUDA(cudaMemsetAsync(b.count, 0, sizeof(unsigned long long), s));
-      k_mine_tasks<<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
-                                                      b, g->bloom_lists.as<int32_t>(), g->split_win.as<int4>(),
-                                                      gate);
-      TM_LAUNCHED("k_mine_tasks");
+      if (split_tasks) {
+        // item tasks defer their chain descents to records; chain tasks and
+        // the records (which may emit chain tasks for the next round) follow
+        TM_CUDA(cudaMemsetAsync(cq.count, 0, sizeof(unsigned long long), s));
+        Queue bd = b;
+        bd.chains = cq;
+        k_mine_tasks<1><<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
+                                                           bd, g->bloom_lists.as<int32_t>(),
+                                                           g->split_win.as<int4>(), nullptr);
+        TM_LAUNCHED("k_mine_tasks");
+        k_mine_tasks<2><<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
+                                                           b, g->bloom_lists.as<int32_t>(),
+                                                           g->split_win.as<int4>(), nullptr);
+        TM_LAUNCHED("k_mine_tasks");
+        k_mine_chains<<<148 * 8, 256, 0, s>>>(dg, dpp, lo + r0, po, cq, b);
+        TM_LAUNCHED("k_mine_chains");
+      } else {
+        k_mine_tasks<0><<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
+                                                           b, g->bloom_lists.as<int32_t>(),
+                                                           g->split_win.as<int4>(), gate);
+        TM_LAUNCHED("k_mine_tasks");
+      }
       std::swap(a, b);
     }
     if (rounds > 0) {

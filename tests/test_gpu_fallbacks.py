@@ -28,11 +28,14 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-def test_tiny_caps_variant_is_exact_and_hits_every_fallback():
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_tiny_caps_variant_is_exact_and_hits_every_fallback(split):
+    """split=1: item tasks defer their chain descents too (the big-call
+    path, TM_SPLIT_TASKS) — their records overflow the tiny chain queue."""
     from paper_2604_12241_b200 import build
     lib = build.TINY_LIB
     assert lib.exists(), "build() makes the tiny-caps test variant"
-    env = dict(os.environ, TM_LIB=str(lib))
+    env = dict(os.environ, TM_LIB=str(lib), TM_SPLIT_TASKS=split)
     res = subprocess.run([sys.executable, str(ROOT / "tests" / "_fallback_worker.py")], env=env,
                          capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stderr[-4000:]
