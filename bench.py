@@ -517,6 +517,7 @@ def main():
     if not a.no_e2e:
         from types import SimpleNamespace
 
+        from paper_2604_12241_b200 import hostmem
         from paper_2604_12241_b200.distributed import mine_distributed
         lab = np.full(E, -1, dtype=np.int8)
         e2e_ms = []
@@ -545,6 +546,7 @@ def main():
                "d2h_bytes_per_step": 8 * E * C * world, "ms_per_step": em, "median_ms": med,
                "median_value": E / (med / 1e3), "max_over_median": float(np.max(e2e_ms)) / med,
                "step_ms": [round(x, 3) for x in e2e_ms],
+               "pinned_pool": dict(hostmem.stats),
                "api": "paper_2604_12241_b200.mine(graph, plans)" if world == 1 else
                       "paper_2604_12241_b200.distributed.mine_distributed(graph, plans)",
                "includes": "H2D of src/dst/time (pinned), GPU CSR build, mining, D2H of the int64 "

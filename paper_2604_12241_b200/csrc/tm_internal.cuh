@@ -90,6 +90,9 @@ struct CycGroup {
   int32_t deep_split;      // chain nodes with wider windows leave the warp kernel (pull tasks)
 };
 
+constexpr int kLaneCyc2 = 1 << 8;   // lane_d kind: cycle_2 (else FAN / DEGREE)
+constexpr int kLaneStack = 1 << 8;  // end_d kind: stack (else cycle_3)
+
 // the columns sharing one delta: one set of trigger windows, one
 // lower-bound table, one pass over each trigger slice
 struct DevGroup {
@@ -111,6 +114,14 @@ struct DevGroup {
   int32_t has_stack;
   int32_t ncols, n_sg, n_gs;
   int8_t cols[kMaxPlans];
+  // the lane-owned columns in two packed lists (the trigger kernel walks
+  // these instead of every column's DevPlan): FAN / DEGREE / cycle_2 right
+  // after the windows, stack / cycle_3 after the items.  lane_d = column |
+  // kind << 8 | endpoint << 10 | direction << 11 | exclude_trigger << 12;
+  // lane_k = min_size
+  int32_t n_lane, n_end;
+  int32_t lane_d[kMaxPlans], lane_k[kMaxPlans];
+  int32_t end_d[kMaxPlans], end_k[kMaxPlans];
   int8_t sg_col[kMaxPlans];
   int8_t gs_col[kMaxPlans];
   CycGroup cyc;

@@ -670,8 +670,11 @@ __device__ __forceinline__ void flat_for(WarpShared &ws, int lane, int len, F &&
 #ifndef TM_WARP_MINB_DEFER  // the same with deferred chain descents (48 registers, no spills)
 #define TM_WARP_MINB_DEFER 20
 #endif
+#ifndef TM_ONE_GROUP  // 1: calls with one delta group run a kernel instance whose group is
+#define TM_ONE_GROUP 1   // P.gr[0] at compile time (constant-bank operands instead of indexed loads)
+#endif
 // one block's 64 triggers (virtual block vb of the call)
-template <bool DEFER>
+template <bool DEFER, bool ONE>
 __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P, int64_t lo, int64_t n_rows,
                                            long long *__restrict__ out, const Queue &qu,
                                            int32_t *__restrict__ split_rows, int32_t *__restrict__ split_n,
@@ -701,8 +704,9 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
   if (valid) TM_CNT(kCtrTrig, 1);
   long long *orow = out + row * C;  // the lane's own row (valid lanes only)
 
-  for (int gi = 0; gi < P.ngroups; ++gi) {
-    const DevGroup &gr = P.gr[gi];
+  const int ngroups = ONE ? 1 : P.ngroups;
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const DevGroup &gr = P.gr[ONE ? 0 : gi];
     int slab = 0;
     uint32_t wlo = 1u;
     if (valid) {
@@ -721,19 +725,19 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
     if (valid) trigger_windows(c, gr, (int)row);
     // per-lane columns: fan / degree (kernels.py:290-303), cycle_2 (:320-322)
     if (valid) {
-      for (int i = 0; i < gr.ncols; ++i) {
-        const int ci = gr.cols[i];
-        const DevPlan &p = P.p[ci];
-        if (p.family == TM_FAN || p.family == TM_DEGREE) {
-          const int x = p.endpoint ? v : u;
-          const Win w = p.endpoint ? (p.direction ? c.wvo : c.wvi) : (p.direction ? c.wuo : c.wui);
-          long long n = w.len() - loops_in_window(c, x, p.endpoint ? loop_v : loop_u);
-          if (p.exclude_trigger && u != v) n -= 1;
-          if (p.min_size > 1 && n < p.min_size) n = 0;
-          orow[ci] = n;
-        } else if (p.family == TM_CYCLE && p.cycle_len == 2) {
+      for (int i = 0; i < gr.n_lane; ++i) {
+        const int d = gr.lane_d[i], ci = d & 0xff;
+        const long long k = gr.lane_k[i];
+        if (d & kLaneCyc2) {
           const long long raw = (u != v && exists_in(c, 1, v, c.wvo, u)) ? 1 : 0;
-          orow[ci] = raw >= p.min_size ? raw : 0;
+          orow[ci] = raw >= k ? raw : 0LL;
+        } else {
+          const bool ep = (d >> 10) & 1, dir = (d >> 11) & 1;
+          const Win w = ep ? (dir ? c.wvo : c.wvi) : (dir ? c.wuo : c.wui);
+          long long n = w.len() - loops_in_window(c, ep ? v : u, ep ? loop_v : loop_u);
+          if (((d >> 12) & 1) && u != v) n -= 1;
+          if (k > 1 && n < k) n = 0;
+          orow[ci] = n;
         }
       }
     }
@@ -805,13 +809,13 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
         scratch[3 * slot + 1] = (int)d;
         scratch[3 * slot + 2] = (int)c3;
       }
-      for (int i = 0; i < gr.ncols; ++i) {
-        const int ci = gr.cols[i];
-        const DevPlan &p = P.p[ci];
-        if (p.family == TM_STACK)
-          orow[ci] = (a > 0 && d > 0 && a >= p.min_size && d >= p.min_size) ? a * d : 0;
-        else if (p.family == TM_CYCLE && p.cycle_len == 3)
-          orow[ci] = c3 >= p.min_size ? c3 : 0;
+      for (int i = 0; i < gr.n_end; ++i) {
+        const int dd = gr.end_d[i], ci = dd & 0xff;
+        const long long k = gr.end_k[i];
+        if (dd & kLaneStack)
+          orow[ci] = (a > 0 && d > 0 && a >= k && d >= k) ? a * d : 0LL;
+        else
+          orow[ci] = c3 >= k ? c3 : 0LL;
       }
     }
     __syncwarp();
@@ -841,7 +845,7 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
 // The trigger kernel.  gate != null (the rescue pass): a small grid that
 // exits at once unless the deferred pass overflowed; virtual blocks are
 // strided over the grid, so the rescue needs no full-size launch.
-template <bool DEFER>
+template <bool DEFER, bool ONE>
 __global__ void __launch_bounds__(kThreads, DEFER ? TM_WARP_MINB_DEFER : TM_WARP_MINB) k_mine_warp(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     int64_t n_rows, long long *__restrict__ out, Queue qu, int32_t *__restrict__ split_rows,
@@ -853,7 +857,7 @@ __global__ void __launch_bounds__(kThreads, DEFER ? TM_WARP_MINB_DEFER : TM_WARP
   __shared__ WarpShared wsh[kWarps];
   const int64_t nvb = (n_rows + kThreads - 1) / kThreads;
   for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
-    mine_block<DEFER>(g, P, lo, n_rows, out, qu, split_rows, split_n, scratch, split_win, split_cap, order, vb,
+    mine_block<DEFER, ONE>(g, P, lo, n_rows, out, qu, split_rows, split_n, scratch, split_win, split_cap, order, vb,
                       stage_all, wsh);
     if (vb + gridDim.x < nvb) __syncthreads();  // the next virtual block re-uses the shared state
   }
@@ -1442,6 +1446,16 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
     dp.p[i] = DevPlan{p.family, p.endpoint, p.direction, p.exclude_trigger, p.cycle_len, p.min_size, k};
     DevGroup &gr = dp.gr[k];
     gr.cols[gr.ncols++] = (int8_t)i;
+    {
+      const int packed = i | p.endpoint << 10 | p.direction << 11 | (p.exclude_trigger ? 1 : 0) << 12;
+      if (p.family == TM_FAN || p.family == TM_DEGREE || (p.family == TM_CYCLE && p.cycle_len == 2)) {
+        gr.lane_d[gr.n_lane] = packed | (p.family == TM_CYCLE ? kLaneCyc2 : 0);
+        gr.lane_k[gr.n_lane++] = p.min_size;
+      } else if (p.family == TM_STACK || (p.family == TM_CYCLE && p.cycle_len == 3)) {
+        gr.end_d[gr.n_end] = packed | (p.family == TM_STACK ? kLaneStack : 0);
+        gr.end_k[gr.n_end++] = p.min_size;
+      }
+    }
     switch (p.family) {
       case TM_FAN:
       case TM_DEGREE: gr.need |= 1 << (2 * p.endpoint + p.direction); break;
@@ -1616,14 +1630,16 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
   }
   const size_t smem = sizeof(long long) * kThreads * std::max(dp.n_stage, 1);
   if (smem > 48 * 1024)
-    for (const void *kf : {(const void *)k_mine_warp<true>, (const void *)k_mine_warp<false>})
+    for (const void *kf : {(const void *)k_mine_warp<true, false>, (const void *)k_mine_warp<true, true>,
+                           (const void *)k_mine_warp<false, false>})
       TM_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // TM_CARVEOUT=pct: preferred shared-memory share of the L1/shared array
   // for the mining kernels (A/B: the walkers' loads are L1-cached)
   if (const char *co = getenv("TM_CARVEOUT")) {
     const int pct = atoi(co);
-    TM_CUDA(cudaFuncSetAttribute(k_mine_warp<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    TM_CUDA(cudaFuncSetAttribute(k_mine_warp<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    TM_CUDA(cudaFuncSetAttribute(k_mine_warp<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    TM_CUDA(cudaFuncSetAttribute(k_mine_warp<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    TM_CUDA(cudaFuncSetAttribute(k_mine_warp<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     for (const void *kf : {(const void *)k_mine_tasks<0>, (const void *)k_mine_tasks<1>, (const void *)k_mine_tasks<2>})
       TM_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   }
@@ -1681,7 +1697,8 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
     if (defer) {
       Queue aw = a;
       aw.chains = cq;
-      k_mine_warp<true><<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
+      auto warp_kernel = (TM_ONE_GROUP && dp.ngroups == 1) ? k_mine_warp<true, true> : k_mine_warp<true, false>;
+      warp_kernel<<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
           dg, dpp, lo + r0, r1 - r0, po, aw, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
           g->split_win.as<int4>(), (int32_t)split_cap, order, nullptr);
       TM_LAUNCHED("k_mine_warp");
@@ -1691,7 +1708,7 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
       // the gated rescue pass: a resident-size grid strides over the rows
       const unsigned grid = gate ? std::min<unsigned>(grid_for(r1 - r0, kThreads), 148 * 16)
                                  : grid_for(r1 - r0, kThreads);
-      k_mine_warp<false><<<grid, kThreads, smem, s>>>(
+      k_mine_warp<false, false><<<grid, kThreads, smem, s>>>(
           dg, dpp, lo + r0, r1 - r0, po, a, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
           g->split_win.as<int4>(), (int32_t)split_cap, order, gate);
       TM_LAUNCHED("k_mine_warp");

@@ -23,6 +23,7 @@ from . import _lib
 KEEP_BLOCKS = 2  # freed blocks kept for re-use
 
 _pool: list[tuple[int, int]] = []  # (capacity bytes, pointer)
+stats = {"fresh": 0, "reused": 0, "returned": 0}  # block counters (diagnostics)
 _lock = threading.Lock()
 
 
@@ -42,6 +43,7 @@ class _Block:
 
 def _release(ptr: int, nbytes: int) -> None:
     with _lock:
+        stats["returned"] += 1
         _pool.append((nbytes, ptr))
         _pool.sort()
         while len(_pool) > KEEP_BLOCKS:
@@ -71,6 +73,9 @@ def pinned_empty(shape: tuple, dtype=np.int64) -> np.ndarray:
         if lib.tm_host_alloc(n, ctypes.byref(p)) != _lib.TM_OK or not p.value:
             return np.empty(shape, dtype=dtype)
         got = (n, p.value)
+        stats["fresh"] += 1
+    else:
+        stats["reused"] += 1
     cap, ptr = got
     blk = _Block(ptr, cap)
     fin = weakref.finalize(blk, _release, ptr, cap)

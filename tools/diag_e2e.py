@@ -14,6 +14,16 @@ if len(sys.argv) > 3:
 import paper_2604_12241_b200 as tmb  # noqa: E402
 from paper_2604_12241_b200 import synth  # noqa: E402
 
+if os.environ.get("TM_BIND") == "1":  # pin the process to the GPU's NUMA-local cores
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(0)
+    words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+    cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+    cpus &= os.sched_getaffinity(0)
+    if cpus:
+        os.sched_setaffinity(0, cpus)
+    print(f"bound to {len(cpus)} cpus: {sorted(cpus)[:4]}...", flush=True)
 name = sys.argv[1] if len(sys.argv) > 1 else "hi-small"
 g0 = synth.time_ordered(synth.generate(synth.CONFIGS[name]))
 pin = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).pin_memory().numpy()
@@ -44,5 +54,7 @@ for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 4):
     fm.device_graph.free()
     del fm, hg
     t3 = time.perf_counter()
+    from paper_2604_12241_b200 import hostmem
+    print(f"pool {hostmem.stats} ", end="")
     print(f"mine() rep {rep}: as_device_graph {1e3*(t1-t0):7.2f} ms  mine {1e3*(t2-t1):7.2f} ms  "
           f"free+del {1e3*(t3-t2):6.2f} ms  total {1e3*(t3-t0):7.2f} ms", flush=True)
