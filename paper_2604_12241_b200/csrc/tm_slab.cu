@@ -76,6 +76,30 @@ __global__ void k_slab_of(const uint32_t *__restrict__ S, int n_slabs, int64_t R
   slab_of[r] = (uint16_t)a;
 }
 
+// The slab of a rank from the slab starts staged in shared memory instead
+// of the rank-indexed slab_of table: global slots are (owner, rank)-sorted,
+// so slab_of[rank] is a random 2-byte load (a DRAM sector per slot) in the
+// build kernels.  sS[i] = S[sb + i] for slabs sb .. s1 + 1; the result is
+// the last s in [sb, s1] with S[s] <= r (callers pass r >= S[sb]).
+#ifndef TM_SLAB_SEARCH
+#define TM_SLAB_SEARCH 1
+#endif
+__device__ __forceinline__ int slab_in_smem(const uint32_t *sS, int sb, int s1, uint32_t r) {
+  int a = 0, b = s1 - sb + 1;  // answer index in [a, b)
+  while (b - a > 1) {
+    const int m = (a + b) >> 1;
+    if (sS[m] <= r) a = m; else b = m;
+  }
+  return sb + a;
+}
+// stage S[sb .. s1 + 1] (sb = max(s0 - 1, 0): a slot's home slab can be the
+// one before s0 when only its halo copy is built)
+__device__ __forceinline__ int stage_slab_starts(uint32_t *sS, const uint32_t *__restrict__ S, int s0, int s1) {
+  const int sb = s0 > 0 ? s0 - 1 : 0;
+  for (int i = threadIdx.x; i <= s1 + 1 - sb; i += blockDim.x) sS[i] = __ldg(S + sb + i);
+  return sb;
+}
+
 // slab s holds global slot j (rank r) iff L_s <= r < S_{s+1}; the slabs of
 // r are [slab_of(r), ...) while L_s <= r (two at most when W >= delta).
 // Cells are owner-major: cell (x, s) = x * ns + s.
@@ -87,8 +111,13 @@ __device__ __forceinline__ void slab_edge_slot(int64_t j, uint32_t r, const int3
                                                const uint32_t *__restrict__ rnk, const int32_t *__restrict__ ptr,
                                                int s0, int s1, const uint16_t *__restrict__ slab_of,
                                                const uint32_t *__restrict__ S, const uint32_t *__restrict__ L,
-                                               int32_t *__restrict__ startT, int32_t *__restrict__ endT) {
+                                               int32_t *__restrict__ startT, int32_t *__restrict__ endT,
+                                               const uint32_t *sS, int sb) {
+#if TM_SLAB_SEARCH
+  int s = slab_in_smem(sS, sb, s1, r);
+#else
   int s = __ldg(slab_of + r);
+#endif
   const int x = __ldg(owner + j);
   const int a = __ldg(ptr + x), b = __ldg(ptr + x + 1);
   const uint32_t rp = j > a ? __ldg(rnk + j - 1) : 0u;
@@ -106,6 +135,9 @@ __global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *
                              const uint16_t *__restrict__ slab_of, const uint32_t *__restrict__ S,
                              const uint32_t *__restrict__ L, int32_t *__restrict__ startT,
                              int32_t *__restrict__ endT) {
+  __shared__ uint32_t sS[kMaxSlabs + 2];
+  const int sb = stage_slab_starts(sS, S, s0, s1);
+  __syncthreads();
   const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= E) return;
   const uint32_t r_lo = __ldg(L + s0), r_hi = __ldg(S + s1 + 1);  // ranks held by slabs s0..s1
@@ -120,7 +152,7 @@ __global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     if (j0 + k < E && r4[k] >= r_lo && r4[k] < r_hi)
-      slab_edge_slot(j0 + k, r4[k], owner, rnk, ptr, s0, s1, slab_of, S, L, startT, endT);
+      slab_edge_slot(j0 + k, r4[k], owner, rnk, ptr, s0, s1, slab_of, S, L, startT, endT, sS, sb);
 }
 
 // The slab-major offsets ptrS[s][x] = (entries of slabs < s) + (entries of
@@ -217,6 +249,8 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
   uint32_t *b_rk = reinterpret_cast<uint32_t *>(b_np + kFillItems);      // [kFillItems]
   int32_t *b_dst = reinterpret_cast<int32_t *>(b_rk + kFillItems);       // [kFillItems]
   __shared__ int32_t cnt[kMaxSlabBins], first[kMaxSlabBins], off[kMaxSlabBins + 1];
+  __shared__ uint32_t sS[kMaxSlabBins + 2];
+  const int sb = stage_slab_starts(sS, S_next - 1, s0, s1);
   for (int i = threadIdx.x; i < ns; i += kFillThreads) {
     cnt[i] = 0;
     first[i] = INT32_MAX;
@@ -237,7 +271,11 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
     if (j < E) {
       r[k] = __ldg(rnk + j);
       if (r[k] < r_lo || r[k] >= r_hi) continue;  // in no built slab
+#if TM_SLAB_SEARCH
+      const int s = slab_in_smem(sS, sb, s1, r[k]);
+#else
       const int s = __ldg(slab_of + r[k]);
+#endif
       // copies in slabs s (home) and s + 1 (inside its halo), clipped to [s0, s1]
       const bool home = s >= s0 && s <= s1;
       const bool next = s + 1 >= s0 && s + 1 <= s1 && __ldg(L + s + 1) <= r[k];
