@@ -155,6 +155,22 @@ __device__ __forceinline__ bool bloom_has(const uint32_t *w, int x) {
   return (w[b >> 5] >> (b & 31)) & 1u;
 }
 
+#ifndef TM_WARM_ROLL  // 1: the trigger kernel's short per-column loops stay rolled (smaller code)
+#define TM_WARM_ROLL 1
+#endif
+#if TM_WARM_ROLL
+#define TM_WARM_ROLLED _Pragma("unroll 1")
+#else
+#define TM_WARM_ROLLED
+#endif
+#ifndef TM_EMIT_NOINLINE  // 1: task emission out of line (cold: 0.006 tasks per trigger)
+#define TM_EMIT_NOINLINE 0
+#endif
+#if TM_EMIT_NOINLINE
+#define TM_EMIT_ATTR __noinline__
+#else
+#define TM_EMIT_ATTR
+#endif
 // reserve n slots of the queue, or none (-1).  The count is 64-bit, so the
 // increments of reservations that fail past a full queue cannot wrap it into
 // a small (or negative) index; a failed reservation that straddles the end
@@ -166,6 +182,7 @@ __device__ __forceinline__ int reserve(const Queue &qu, int n) {
   if (*(volatile unsigned long long *)qu.count >= cap) return -1;
   const unsigned long long base = atomicAdd(qu.count, (unsigned long long)n);
   if (base + (unsigned long long)n > cap) {
+#pragma unroll 1  // cold path: keep it out of the hot kernels' instruction footprint
     for (unsigned long long k = base; k < cap; ++k) qu.q[k].row = -1;  // holes stay empty
     return -1;
   }
@@ -174,7 +191,7 @@ __device__ __forceinline__ int reserve(const Queue &qu, int n) {
 
 // cut [a, b) into kTaskSpan pieces; false (caller walks it itself) when the
 // queue is full — the walk is slower but exact and still on the GPU
-__device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p1, int p2, int p3,
+__device__ TM_EMIT_ATTR bool emit(const Queue &qu, int row, int grp, int level, int p0, int p1, int p2, int p3,
                      int p4, int a, int b, int parts = kVAll) {
   const int n = (b - a + kTaskSpan - 1) / kTaskSpan;
   TM_CNT(level >= kLvlDomU ? kCtrDomTask : kCtrChainTask, n);
@@ -183,6 +200,7 @@ __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p
     TM_CNT(kCtrQueueFull, 1);
     return false;
   }
+#pragma unroll 1
   for (int k = 0; k < n; ++k) {
     Task t;
     t.row = row;
@@ -199,7 +217,7 @@ __device__ bool emit(const Queue &qu, int row, int grp, int level, int p0, int p
 }
 
 // one task for the whole range [a, b) (a pull task): false when the queue is full
-__device__ bool emit_whole(const Queue &qu, int row, int grp, int level, const int (&path)[kMaxChain],
+__device__ TM_EMIT_ATTR bool emit_whole(const Queue &qu, int row, int grp, int level, const int (&path)[kMaxChain],
                            int a, int b) {
   TM_CNT(kCtrChainTask, 1);
   const int k = reserve(qu, 1);
@@ -700,6 +718,7 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
     v = __ldg(g.e_dst + e);
     r = __ldg(g.e_rank + e);
   }
+  TM_WARM_ROLLED
   for (int i = 0; i < S; ++i) stage[lane * S + i] = 0;
   if (valid) TM_CNT(kCtrTrig, 1);
   long long *orow = out + row * C;  // the lane's own row (valid lanes only)
@@ -725,6 +744,7 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
     if (valid) trigger_windows(c, gr, (int)row);
     // per-lane columns: fan / degree (kernels.py:290-303), cycle_2 (:320-322)
     if (valid) {
+      TM_WARM_ROLLED
       for (int i = 0; i < gr.n_lane; ++i) {
         const int d = gr.lane_d[i], ci = d & 0xff;
         const long long k = gr.lane_k[i];
@@ -809,6 +829,7 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
         scratch[3 * slot + 1] = (int)d;
         scratch[3 * slot + 2] = (int)c3;
       }
+      TM_WARM_ROLLED
       for (int i = 0; i < gr.n_end; ++i) {
         const int dd = gr.end_d[i], ci = dd & 0xff;
         const long long k = gr.end_k[i];
@@ -823,6 +844,7 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
   __syncwarp();
   if (order) {  // permuted rows: each lane writes its own
     if (valid)
+#pragma unroll 1
       for (int i = 0; i < S; ++i) orow[P.slot_col[i]] = stage[lane * S + i];
     return;
   }
@@ -834,6 +856,7 @@ __device__ __forceinline__ void mine_block(const DevGraph &g, const DevPlans &P,
   // incrementally instead of dividing by the runtime S
   const int dq = 32 / S, dr = 32 % S;
   int r0 = lane / S, k0 = lane % S;
+  TM_WARM_ROLLED
   for (int i = lane; i < nrow * S; i += 32) {
     dst[r0 * C + P.slot_col[k0]] = stage[i];
     r0 += dq;
