@@ -81,6 +81,12 @@ __global__ void k_slab_of(const uint32_t *__restrict__ S, int n_slabs, int64_t R
 // so slab_of[rank] is a random 2-byte load (a DRAM sector per slot) in the
 // build kernels.  sS[i] = S[sb + i] for slabs sb .. s1 + 1; the result is
 // the last s in [sb, s1] with S[s] <= r (callers pass r >= S[sb]).
+#ifndef TM_EDGES_HOIST  // 1: full-view edge passes load the 4 owners with the 4 ranks
+#define TM_EDGES_HOIST 1
+#endif
+#ifndef TM_FILL_HOIST  // 1: full-view fills load owner / (nbr, prev) with the rank
+#define TM_FILL_HOIST 1
+#endif
 #ifndef TM_SLAB_SEARCH
 #define TM_SLAB_SEARCH 1
 #endif
@@ -112,13 +118,13 @@ __device__ __forceinline__ void slab_edge_slot(int64_t j, uint32_t r, const int3
                                                int s0, int s1, const uint16_t *__restrict__ slab_of,
                                                const uint32_t *__restrict__ S, const uint32_t *__restrict__ L,
                                                int32_t *__restrict__ startT, int32_t *__restrict__ endT,
-                                               const uint32_t *sS, int sb) {
+                                               const uint32_t *sS, int sb, int x) {
 #if TM_SLAB_SEARCH
   int s = slab_in_smem(sS, sb, s1, r);
 #else
   int s = __ldg(slab_of + r);
 #endif
-  const int x = __ldg(owner + j);
+  if (x < 0) x = __ldg(owner + j);
   const int a = __ldg(ptr + x), b = __ldg(ptr + x + 1);
   const uint32_t rp = j > a ? __ldg(rnk + j - 1) : 0u;
   const uint32_t rn = j + 1 < b ? __ldg(rnk + j + 1) : 0xffffffffu;
@@ -142,9 +148,14 @@ __global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *
   if (j0 >= E) return;
   const uint32_t r_lo = __ldg(L + s0), r_hi = __ldg(S + s1 + 1);  // ranks held by slabs s0..s1
   uint32_t r4[4];
+  int x4[4] = {-1, -1, -1, -1};  // owners (-1: loaded per slot)
   if (j0 + 4 <= E) {  // rank arrays are 16-byte aligned (device buffers)
     const uint4 q = __ldg(reinterpret_cast<const uint4 *>(rnk + j0));
     r4[0] = q.x; r4[1] = q.y; r4[2] = q.z; r4[3] = q.w;
+    if (TM_EDGES_HOIST && s0 == 0) {  // a full view: every slot is in range
+      const int4 o = __ldg(reinterpret_cast<const int4 *>(owner + j0));
+      x4[0] = o.x; x4[1] = o.y; x4[2] = o.z; x4[3] = o.w;
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k) r4[k] = j0 + k < E ? __ldg(rnk + j0 + k) : 0xffffffffu;
@@ -152,7 +163,7 @@ __global__ void k_slab_edges(const int32_t *__restrict__ owner, const uint32_t *
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     if (j0 + k < E && r4[k] >= r_lo && r4[k] < r_hi)
-      slab_edge_slot(j0 + k, r4[k], owner, rnk, ptr, s0, s1, slab_of, S, L, startT, endT, sS, sb);
+      slab_edge_slot(j0 + k, r4[k], owner, rnk, ptr, s0, s1, slab_of, S, L, startT, endT, sS, sb, x4[k]);
 }
 
 // The slab-major offsets ptrS[s][x] = (entries of slabs < s) + (entries of
@@ -264,12 +275,24 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
   int2 e[kFillPer];
   uint32_t r[kFillPer];
   int b0[kFillPer], d0[kFillPer], d1[kFillPer];  // bin of the first copy, its / the next bin's destination
+  int xo[kFillPer];
+  // a full view (s0 == 0) copies every slot: its owner and (nbr, prev) are
+  // loaded with its rank, off the rank -> slab -> offset chain
+  const bool hoist = TM_FILL_HOIST && s0 == 0;
+#pragma unroll
+  for (int k = 0; k < kFillPer; ++k) {
+    const int64_t j = base + k * kFillThreads + threadIdx.x;
+    r[k] = j < E ? __ldg(rnk + j) : 0xffffffffu;
+    if (hoist && j < E) {
+      xo[k] = __ldg(owner + j);
+      e[k] = __ldg(np + j);
+    }
+  }
 #pragma unroll
   for (int k = 0; k < kFillPer; ++k) {
     const int64_t j = base + k * kFillThreads + threadIdx.x;
     b0[k] = -1;
     if (j < E) {
-      r[k] = __ldg(rnk + j);
       if (r[k] < r_lo || r[k] >= r_hi) continue;  // in no built slab
 #if TM_SLAB_SEARCH
       const int s = slab_in_smem(sS, sb, s1, r[k]);
@@ -280,8 +303,13 @@ __global__ void __launch_bounds__(kFillThreads) k_slab_fill(
       const bool home = s >= s0 && s <= s1;
       const bool next = s + 1 >= s0 && s + 1 <= s1 && __ldg(L + s + 1) <= r[k];
       if (home || next) {
-        const int x = __ldg(owner + j);
-        e[k] = __ldg(np + j);
+        int x;
+        if (hoist) {
+          x = xo[k];
+        } else {
+          x = __ldg(owner + j);
+          e[k] = __ldg(np + j);
+        }
         const int32_t *dt = deltaT + (int64_t)x * ns - s0;
         if (home) {
           b0[k] = s - s0;
