@@ -1048,7 +1048,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 // and the rescue pass); MODE 1: the item kinds (domain U / V, pull-V) with
 // their chain descents deferred to records (no chain code in this kernel:
 // fewer registers, no Bloom build); MODE 2: the chain kinds only.
-template <int MODE>
+template <int MODE, bool ONE = false>
 __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const __grid_constant__ DevGraph g, const __grid_constant__ DevPlans P, int64_t lo,
     long long *__restrict__ out, int32_t *__restrict__ scratch, Queue in, Queue next_q,
@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
     const bool item_task = t.level == kLvlDomU || t.level == kLvlDomV || t.level == kLvlPullV;
     if ((MODE == 1 && !item_task) || (MODE == 2 && item_task)) continue;
     const int e = (int)(lo + t.row);
-    const DevGroup &gr = P.gr[t.grp];
+    const DevGroup &gr = P.gr[ONE ? 0 : t.grp];
     const uint32_t r = __ldg(g.e_rank + e);
     Ctx c{gr.view, __ldg(g.e_src + e), __ldg(g.e_dst + e), __ldg(gr.lo_tab + r), r, {}, {}, {}, {},
           (int64_t)slab_of(gr, r) * gr.stride};
@@ -1226,6 +1226,7 @@ __global__ void __launch_bounds__(kTaskThreads, TM_TASK_MINB) k_mine_tasks(
 // a1 are enumerated with the task-kernel semantics (wide nodes: pull
 // candidates or chain tasks for the rounds that follow), counts are added
 // to the trigger's row
+template <bool ONE = false>
 __global__ void __launch_bounds__(256) k_mine_chains(const __grid_constant__ DevGraph g,
                                                      const __grid_constant__ DevPlans P, int64_t lo,
                                                      long long *__restrict__ out, ChainQ cq, Queue qu) {
@@ -1233,7 +1234,7 @@ __global__ void __launch_bounds__(256) k_mine_chains(const __grid_constant__ Dev
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const ChainRec rc = cq.rec[i];
-    const DevGroup &gr = P.gr[rc.grp];
+    const DevGroup &gr = P.gr[ONE ? 0 : rc.grp];
     const int e = (int)(lo + rc.row);
     const uint32_t r = __ldg(g.e_rank + e);
     uint32_t wlo;
@@ -1652,6 +1653,8 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
     if (staged) dp.slot_col[dp.n_stage++] = (int8_t)i;
   }
   const size_t smem = sizeof(long long) * kThreads * std::max(dp.n_stage, 1);
+  // one delta group (the common case): kernel instances with P.gr[0] fixed
+  const bool one_group = TM_ONE_GROUP && dp.ngroups == 1;
   if (smem > 48 * 1024)
     for (const void *kf : {(const void *)k_mine_warp<true, false>, (const void *)k_mine_warp<true, true>,
                            (const void *)k_mine_warp<false, false>})
@@ -1663,7 +1666,8 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     TM_CUDA(cudaFuncSetAttribute(k_mine_warp<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    for (const void *kf : {(const void *)k_mine_tasks<0>, (const void *)k_mine_tasks<1>, (const void *)k_mine_tasks<2>})
+    for (const void *kf : {(const void *)k_mine_tasks<0>, (const void *)k_mine_tasks<1>, (const void *)k_mine_tasks<2>,
+                           (const void *)k_mine_tasks<1, true>, (const void *)k_mine_tasks<2, true>})
       TM_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   }
   // Host output: mine the range in pieces and copy each finished piece back
@@ -1720,12 +1724,12 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
     if (defer) {
       Queue aw = a;
       aw.chains = cq;
-      auto warp_kernel = (TM_ONE_GROUP && dp.ngroups == 1) ? k_mine_warp<true, true> : k_mine_warp<true, false>;
+      auto warp_kernel = one_group ? k_mine_warp<true, true> : k_mine_warp<true, false>;
       warp_kernel<<<grid_for(r1 - r0, kThreads), kThreads, smem, s>>>(
           dg, dpp, lo + r0, r1 - r0, po, aw, g->heavy_q.as<int32_t>(), cnt, g->split_scratch.as<int32_t>(),
           g->split_win.as<int4>(), (int32_t)split_cap, order, nullptr);
       TM_LAUNCHED("k_mine_warp");
-      k_mine_chains<<<148 * 8, 256, 0, s>>>(dg, dpp, lo + r0, po, cq, a);
+      (one_group ? k_mine_chains<true> : k_mine_chains<false>)<<<148 * 8, 256, 0, s>>>(dg, dpp, lo + r0, po, cq, a);
       TM_LAUNCHED("k_mine_chains");
     } else {
       // the gated rescue pass: a resident-size grid strides over the rows
@@ -1749,15 +1753,17 @@ static int mine_impl(tm_graph *g, const tm_plan_desc *plans, int n_plans, int64_
         TM_CUDA(cudaMemsetAsync(cq.count, 0, sizeof(unsigned long long), s));
         Queue bd = b;
         bd.chains = cq;
-        k_mine_tasks<1><<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
+        (one_group ? k_mine_tasks<1, true> : k_mine_tasks<1, false>)<<<task_grid, kTaskThreads, 0, s>>>(
+            dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
                                                            bd, g->bloom_lists.as<int32_t>(),
                                                            g->split_win.as<int4>(), nullptr);
         TM_LAUNCHED("k_mine_tasks");
-        k_mine_tasks<2><<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
+        (one_group ? k_mine_tasks<2, true> : k_mine_tasks<2, false>)<<<task_grid, kTaskThreads, 0, s>>>(
+            dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
                                                            b, g->bloom_lists.as<int32_t>(),
                                                            g->split_win.as<int4>(), nullptr);
         TM_LAUNCHED("k_mine_tasks");
-        k_mine_chains<<<148 * 8, 256, 0, s>>>(dg, dpp, lo + r0, po, cq, b);
+        (one_group ? k_mine_chains<true> : k_mine_chains<false>)<<<148 * 8, 256, 0, s>>>(dg, dpp, lo + r0, po, cq, b);
         TM_LAUNCHED("k_mine_chains");
       } else {
         k_mine_tasks<0><<<task_grid, kTaskThreads, 0, s>>>(dg, dpp, lo + r0, po, g->split_scratch.as<int32_t>(), a,
